@@ -1,0 +1,142 @@
+/*
+ * tileinv_b200.h -- C ABI of the B200-native tile Cholesky + selected-inversion
+ * path (drop-in for the hot path of the reference `tileinv`, arXiv 2504.19171).
+ *
+ * Plain pointers, sizes and opaque handles only; no C++ or torch types.  Every
+ * call is synchronous and returns a status code (TIB_OK = 0); the message of
+ * the last failure on the calling thread is available from
+ * tib_last_error_message().  Status codes map one-to-one onto the reference's
+ * exception classes (proj/include/tileinv/errors.hpp:8-58) and its Python
+ * translation (proj/bindings/module.cpp:131-132).
+ *
+ * Each entry point names the reference interface it replaces (file:line under
+ * /root/reference/proj).  Device-resident objects (factor, selected inverse)
+ * stay in HBM until freed; host copies are made only on request.
+ */
+#ifndef TILEINV_B200_H
+#define TILEINV_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.hpp:8-58) ------------------------------------ */
+#define TIB_OK 0
+#define TIB_ERR_GENERIC 1          /* tileinv::Error */
+#define TIB_ERR_INVALID_ARGUMENT 2 /* InvalidArgumentError */
+#define TIB_ERR_NOT_SPD 3          /* NotSpdError{pivot, tile_i, tile_j} */
+#define TIB_ERR_SINGULAR_TILE 4    /* SingularTileError */
+#define TIB_ERR_CONTRACT 5         /* ContractError */
+#define TIB_ERR_CONSISTENCY 6      /* ConsistencyError */
+#define TIB_ERR_STRUCTURE 7        /* StructureError */
+#define TIB_ERR_PARSE 8            /* ParseError */
+#define TIB_ERR_FORMAT 9           /* FormatError */
+#define TIB_ERR_CUDA 10            /* device / runtime failure (no reference analogue) */
+
+/* ---- selection presets (selinv.hpp:12-24, module.cpp:34-44) ------------- */
+#define TIB_SELECT_ENTRIES 0  /* explicit (r, c) list */
+#define TIB_SELECT_DIAGONAL 1 /* "diagonal"  */
+#define TIB_SELECT_PATTERN 2  /* "pattern"   */
+#define TIB_SELECT_ALL 3      /* "all"       */
+
+typedef struct tib_matrix_s* tib_matrix; /* TiledSymmetricMatrix (storage.hpp:40-44), host */
+typedef struct tib_factor_s* tib_factor; /* TiledFactor (storage.hpp:46-51), device */
+typedef struct tib_sigma_s* tib_sigma;   /* SelectedInverse (selinv.hpp:61-68), device */
+
+/* ---- library ------------------------------------------------------------ */
+const char* tib_version(void);                 /* version.hpp:5 kVersion */
+const char* tib_last_error_message(void);      /* what() of the last failure */
+/* NotSpdError fields of the last TIB_ERR_NOT_SPD (errors.hpp:38-44). */
+int tib_last_not_spd(long* pivot, int* tile_i, int* tile_j);
+int tib_device_count(int* count);
+
+/* ---- matrices (host side; input formats) --------------------------------- */
+/* generate_arrowhead (matgen.hpp:54, matgen.cpp:59-120), bit-exact values.  */
+int tib_matrix_generate(long n, long bandwidth, long thickness, double density, uint64_t seed,
+                        int tile_size, tib_matrix* out);
+/* from_dense (module.cpp:46-74): row-major n x n, lower triangle read.      */
+int tib_matrix_from_dense(long n, int tile_size, const double* a, tib_matrix* out);
+/* Tiles (i >= j), each b*b row-major, as a TileBlocks payload list.         */
+int tib_matrix_from_tiles(long n, int tile_size, long count, const int* ti, const int* tj,
+                          const double* payload, tib_matrix* out);
+/* read_matrix_market (matgen.cpp:208-319) from a text buffer.                */
+int tib_matrix_read_mm(const char* text, size_t len, int tile_size, tib_matrix* out);
+/* write_matrix_market (matgen.cpp:146-184); *len_inout is the buffer size; on
+ * return the full text size (call with buf = NULL to query).                 */
+int tib_matrix_write_mm(tib_matrix m, char* buf, size_t* len_inout);
+int tib_matrix_info(tib_matrix m, long* n, int* tile_size, int* n_tiles, long* stored_tiles);
+/* stored tiles in column-major tile order; payload is count * b * b doubles */
+int tib_matrix_tiles(tib_matrix m, int* ti, int* tj, double* payload);
+int tib_matrix_free(tib_matrix m);
+
+/* ---- symbolic analysis (layout.cpp, cholesky.cpp:17-49, selinv.cpp:85-150) */
+/* Filled factor pattern of m (symbolic_fill): count, then coordinates.       */
+int tib_symbolic_pattern(tib_matrix m, long* count, int* ti, int* tj);
+/* Closure of a request over the factor pattern (select_tiles +
+ * symbolic_inversion): count, then coordinates; growth_warning optional.    */
+int tib_symbolic_closure(tib_matrix m, int preset, const long* rows, const long* cols,
+                         long nentries, long* count, int* ti, int* tj, int* growth_warning);
+/* Task-model FLOPs of factorize / phase 1 / phase 2.        */
+int tib_flops(tib_matrix m, int preset, const long* rows, const long* cols, long nentries,
+              double* factorize, double* phase1, double* phase2);
+
+/* ---- factorization (cholesky.hpp:28-33, selinv.cpp:195-237) --------------- */
+/* symbolic_cholesky + factorize on `device`.  The factor stays in HBM; the
+ * phase-1 transform (U_j, W_kj) is produced in the same column sweep.  On
+ * TIB_ERR_NOT_SPD, tib_last_not_spd() carries the global pivot and tile.      */
+int tib_factorize(tib_matrix m, int device, tib_factor* out);
+int tib_factor_info(tib_factor f, long* n, int* tile_size, long* stored_tiles);
+/* 2 * sum_r log L_rr (not a reference API).               */
+int tib_factor_logdet(tib_factor f, double* out);
+/* Download L (phase = 1) or the phase-1 tiles U/W (phase = 2), column-major
+ * tile order, b*b row-major each (the reference TileBlocks payload).          */
+int tib_factor_tiles(tib_factor f, int phase, int* ti, int* tj, double* payload);
+/* payload_checksum (storage.cpp:34-48) of the L tiles as stored here.         */
+int tib_factor_checksum(tib_factor f, uint64_t* out);
+int tib_factor_free(tib_factor f);
+
+/* ---- selected inversion (selinv.hpp:70-85) -------------------------------- */
+/* selected_inverse(const TiledSymmetricMatrix&, request, workers)
+ * (selinv.cpp:359-367): factorize -> select -> closure -> phase1 -> phase2.  */
+int tib_selected_inverse(tib_matrix m, int preset, const long* rows, const long* cols,
+                         long nentries, int device, tib_sigma* out);
+/* selected_inverse(const TiledFactor&, request, workers) (selinv.cpp:347-357) */
+int tib_selected_inverse_of_factor(tib_factor f, int preset, const long* rows, const long* cols,
+                                   long nentries, tib_sigma* out);
+int tib_sigma_info(tib_sigma s, long* n, int* tile_size, long* closure_tiles, int* growth_warning);
+/* logdet of the factor the result came from.                                  */
+int tib_sigma_logdet(tib_sigma s, double* out);
+/* Marginal variances diag(Sigma), n doubles (requires the diagonal tiles in
+ * the closure; TIB_ERR_CONTRACT otherwise, like entry_from_closure).          */
+int tib_sigma_diagonal(tib_sigma s, double* out);
+/* extract_entries (selinv.cpp:387-439) for the request the result was built
+ * with: count first (rows/cols/vals NULL), then the entries.                 */
+int tib_sigma_entries(tib_sigma s, long* count, long* rows, long* cols, double* vals);
+/* Closure tiles, column-major tile order, b*b row-major each.                */
+int tib_sigma_tiles(tib_sigma s, int* ti, int* tj, double* payload);
+/* payload_checksum (storage.cpp:34-48) of the result tiles.                   */
+int tib_sigma_checksum(tib_sigma s, uint64_t* out);
+int tib_sigma_free(tib_sigma s);
+
+/* ---- batched selected inversion (INLA hyper-parameter sweeps) -------------- */
+/* count matrices sharing one tile pattern, run as one batched sweep on device:
+ * logdet[count] and diag[count * n] (marginal variances) are written back.   */
+int tib_selected_inverse_batch(const tib_matrix* ms, int count, int device, double* logdet,
+                               double* diag);
+
+/* ---- timing support (bench.py) -------------------------------------------- */
+/* Device-resident run: uploads m once, then `reps` times runs the fused
+ * factorize + selected inversion (pattern) from the resident copy; returns
+ * the per-rep device time in ms (CUDA events on the sweep stream) and the
+ * device time of each sweep phase of the last rep.                            */
+int tib_bench_resident(tib_matrix m, int device, int reps, int warmup, double* ms_per_rep,
+                       double* ms_factor, double* ms_phase2, double* logdet);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TILEINV_B200_H */

@@ -1,0 +1,141 @@
+// Timing / golden driver over the UNMODIFIED reference library (oracle/_ref,
+// built by oracle/Makefile from /root/reference/proj/src).  Test
+// infrastructure: it is the CPU baseline (`cpu_baseline.kind = "reference"`)
+// and the source of golden scalars; the product never links it.
+//
+// It mirrors the reference CLI's timing method (proj/tools/tileinv_main.cpp:
+// 173-203): steady_clock around symbolic_cholesky+factorize, phase1(std::move),
+// and phase2, generation excluded.
+//
+//   ref_driver bench  n w t b seed workers [density]
+//       -> one JSON line {factorize_s, phase1_s, phase2_s, total_s, gflop, ...}
+//   ref_driver dump   n w t b seed workers out_prefix [density]
+//       -> <prefix>.diag.f64 (n doubles), <prefix>.sigma.f64 (closure tiles,
+//          column-major tile order, each b*b row-major) and a JSON line.
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
+#include <string>
+#include <vector>
+
+#include "tileinv/cholesky.hpp"
+#include "tileinv/matgen.hpp"
+#include "tileinv/selinv.hpp"
+
+using namespace tileinv;
+using Clock = std::chrono::steady_clock;
+
+static double secs(Clock::time_point a, Clock::time_point b) {
+  return std::chrono::duration<double>(b - a).count();
+}
+
+struct Flops {
+  double fact = 0, p1 = 0, p2 = 0;
+};
+
+// Task-model FLOPs: POTRF b^3/3, TRSM b^3, SYRK b^3, GEMM 2b^3;
+// TRTRI b^3/3, TRMM b^3; LAUUM b^3/3, GEMM 2b^3 per (target, k) term.
+static Flops count_flops(const FactorPlan& plan, const SelectedTileSet& sel,
+                         const TilePattern& fpat) {
+  const double b = fpat.layout().b, b3 = b * b * b;
+  Flops f;
+  for (const FactorTask& t : plan.tasks) {
+    switch (t.kind) {
+      case FactorKernel::kPotrf: f.fact += b3 / 3; break;
+      case FactorKernel::kTrsm: f.fact += b3; break;
+      case FactorKernel::kSyrk: f.fact += b3; break;
+      case FactorKernel::kGemm: f.fact += 2 * b3; break;
+    }
+  }
+  for (int j = 0; j < fpat.layout().N; ++j) {
+    f.p1 += b3 / 3;
+    for (int i : fpat.neighbors(j))
+      if (i > j) f.p1 += b3;
+  }
+  for (const ColumnWork& c : sel.columns) {
+    int nk = 0;
+    for (int k : fpat.neighbors(c.col))
+      if (k > c.col) ++nk;
+    f.p2 += 2 * b3 * nk * static_cast<double>(c.offdiag_rows.size());
+    if (c.diagonal) f.p2 += b3 / 3 + 2 * b3 * nk;
+  }
+  return f;
+}
+
+int main(int argc, char** argv) {
+  if (argc < 8) {
+    std::fprintf(stderr, "usage: ref_driver bench|dump n w t b seed workers [prefix] [density]\n");
+    return 2;
+  }
+  const std::string mode = argv[1];
+  const long n = std::atol(argv[2]), w = std::atol(argv[3]), t = std::atol(argv[4]);
+  const int b = std::atoi(argv[5]);
+  const unsigned long long seed = std::strtoull(argv[6], nullptr, 10);
+  const int workers = std::atoi(argv[7]);
+  std::string prefix;
+  int argi = 8;
+  if (mode == "dump") prefix = argv[argi++];
+  const double density = argc > argi ? std::atof(argv[argi]) : 1.0;
+
+  const auto g0 = Clock::now();
+  GeneratedMatrix gen = generate_arrowhead({n, w, t, density, seed}, b);
+  const auto g1 = Clock::now();
+
+  const auto t0 = Clock::now();
+  const FactorPlan plan = symbolic_cholesky(gen.matrix.pattern);
+  TiledFactor factor = factorize(gen.matrix, plan, workers);
+  const auto t1 = Clock::now();
+  // logdet is not a reference API: 2 * sum log L_rr, r < n.
+  double logdet = 0.0;
+  for (long r = 0; r < n; ++r) {
+    const auto& d = factor.blocks.at(static_cast<int>(r / b), static_cast<int>(r / b));
+    logdet += 2.0 * std::log(d[static_cast<std::size_t>(r % b) * b + (r % b)]);
+  }
+  const std::uint64_t fsum = payload_checksum(factor.blocks);
+  const std::vector<TileCoord> tiles =
+      select_tiles(factor.layout, factor.pattern, SelectionRequest::factor_pattern());
+  const SelectedTileSet sel = symbolic_inversion(tiles, factor.pattern);
+  const auto t2 = Clock::now();
+  factor = phase1(std::move(factor), workers);
+  const auto t3 = Clock::now();
+  SelectedInverse sigma = phase2(factor, sel, workers);
+  const auto t4 = Clock::now();
+
+  const Flops fl = count_flops(plan, sel, factor.pattern);
+  double trace = 0.0;
+  std::vector<double> diag(static_cast<std::size_t>(n));
+  for (long r = 0; r < n; ++r) {
+    const auto& d = sigma.blocks.at(static_cast<int>(r / b), static_cast<int>(r / b));
+    diag[static_cast<std::size_t>(r)] = d[static_cast<std::size_t>(r % b) * b + (r % b)];
+    trace += diag[static_cast<std::size_t>(r)];
+  }
+  const double total = secs(t0, t1) + secs(t2, t3) + secs(t3, t4);
+  const double gflop = (fl.fact + fl.p1 + fl.p2) / 1e9;
+  std::printf(
+      "{\"n\": %ld, \"w\": %ld, \"t\": %ld, \"b\": %d, \"seed\": %llu, \"workers\": %d, "
+      "\"N\": %d, \"tiles\": %zu, \"closure_tiles\": %zu, \"generate_s\": %.6f, "
+      "\"factorize_s\": %.6f, \"phase1_s\": %.6f, \"phase2_s\": %.6f, \"total_s\": %.6f, "
+      "\"gflop_factorize\": %.6f, \"gflop_phase1\": %.6f, \"gflop_phase2\": %.6f, "
+      "\"gflop\": %.6f, \"gflops\": %.4f, \"logdet\": %.17g, \"trace\": %.17g, "
+      "\"factor_checksum\": %llu, \"result_checksum\": %llu}\n",
+      n, w, t, b, seed, workers, gen.matrix.layout.N, factor.pattern.size(),
+      sigma.closure.size(), secs(g0, g1), secs(t0, t1), secs(t2, t3), secs(t3, t4), total,
+      fl.fact / 1e9, fl.p1 / 1e9, fl.p2 / 1e9, gflop, gflop / total, logdet, trace,
+      static_cast<unsigned long long>(fsum),
+      static_cast<unsigned long long>(payload_checksum(sigma.blocks)));
+
+  if (mode == "dump") {
+    std::ofstream dg(prefix + ".diag.f64", std::ios::binary);
+    dg.write(reinterpret_cast<const char*>(diag.data()),
+             static_cast<std::streamsize>(diag.size() * sizeof(double)));
+    std::ofstream sg(prefix + ".sigma.f64", std::ios::binary);
+    for (const auto& [key, payload] : sigma.blocks.map()) {
+      (void)key;
+      sg.write(reinterpret_cast<const char*>(payload.data()),
+               static_cast<std::streamsize>(payload.size() * sizeof(double)));
+    }
+  }
+  return 0;
+}

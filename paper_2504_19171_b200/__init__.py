@@ -1,0 +1,439 @@
+"""B200-native drop-in for the hot path of ``tileinv`` (arXiv 2504.19171, sTiles).
+
+Same names, argument meaning and error behaviour as the reference Python
+module (proj/bindings/module.cpp:125-237, proj/python/tileinv/__init__.py):
+
+    Matrix, Factor, SelectedInverseResult, TileinvError, NotSpdError,
+    generate, from_dense, read_matrix_market, write_matrix_market,
+    factorize, selected_inverse, selected_inverse_of_factor
+
+Everything numeric runs through the C ABI of ``libtileinv_b200.so``
+(include/tileinv_b200.h): the tile Cholesky, the phase-1 transform and the
+phase-2 Takahashi recursion are sm_100a kernels on the GPU, the factor and
+the result stay resident in HBM.  ``workers`` is accepted for compatibility
+(it must be >= 1, like the reference); ``device`` picks the GPU.
+
+Additions beyond the reference API: ``Factor.logdet()``, ``Factor.tiles()``,
+``SelectedInverseResult.diagonal()`` (marginal variances as a numpy array),
+``.logdet()``, ``.tiles()``, ``selected_inverse_batch`` and the symbolic
+helpers ``factor_pattern`` / ``closure_tiles`` / ``task_flops``.
+
+The DAG analyzer (dag_report / export_dot / predict_gemm_count) is outside
+this path (component 10) and is not provided.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Iterable, Sequence
+
+import numpy as np
+
+from ._lib import lib
+
+__version__ = lib.tib_version().decode()
+
+_PRESETS = {"diagonal": 1, "pattern": 2, "all": 3}
+_ORACLE_LIMIT = 4000  # proj/include/tileinv/oracle.hpp:22
+
+
+class TileinvError(RuntimeError):
+    """Any reference ``tileinv::Error`` (module.cpp:131)."""
+
+
+class NotSpdError(ArithmeticError):
+    """``tileinv::NotSpdError`` (module.cpp:132); carries pivot / tile."""
+
+    def __init__(self, msg: str, pivot: int = -1, tile_i: int = -1, tile_j: int = -1):
+        super().__init__(msg)
+        self.pivot = pivot
+        self.tile_i = tile_i
+        self.tile_j = tile_j
+
+
+def _check(status: int) -> None:
+    if status == 0:
+        return
+    msg = lib.tib_last_error_message().decode(errors="replace")
+    if status == 3:
+        pivot, ti, tj = C.c_long(), C.c_int(), C.c_int()
+        lib.tib_last_not_spd(C.byref(pivot), C.byref(ti), C.byref(tj))
+        raise NotSpdError(msg, pivot.value, ti.value, tj.value)
+    raise TileinvError(msg)
+
+
+def _request(selection) -> tuple[int, np.ndarray | None, np.ndarray | None, int]:
+    """module.cpp:34-44: a preset name or a list of (r, c) pairs."""
+    if isinstance(selection, str):
+        if selection not in _PRESETS:
+            raise ValueError("selection must be 'diagonal', 'pattern', 'all', or a pair list")
+        return _PRESETS[selection], None, None, 0
+    pairs = [(int(r), int(c)) for r, c in selection]
+    rows = np.ascontiguousarray([p[0] for p in pairs], dtype=np.int64)
+    cols = np.ascontiguousarray([p[1] for p in pairs], dtype=np.int64)
+    return 0, rows, cols, len(pairs)
+
+
+def _lp(a):
+    return None if a is None else a.ctypes.data_as(C.POINTER(C.c_long))
+
+
+def _check_workers(workers: int) -> None:
+    if workers < 1:
+        raise TileinvError("worker count must be at least 1")
+
+
+class Matrix:
+    """TiledSymmetricMatrix (storage.hpp:40-44), host resident."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib.tib_matrix_free(h)
+            self._h = None
+
+    def _info(self):
+        n, b, N, s = C.c_long(), C.c_int(), C.c_int(), C.c_long()
+        _check(lib.tib_matrix_info(self._h, C.byref(n), C.byref(b), C.byref(N), C.byref(s)))
+        return n.value, b.value, N.value, s.value
+
+    @property
+    def n(self) -> int:
+        return self._info()[0]
+
+    @property
+    def tile_size(self) -> int:
+        return self._info()[1]
+
+    @property
+    def n_tiles(self) -> int:
+        return self._info()[2]
+
+    @property
+    def stored_tiles(self) -> int:
+        return self._info()[3]
+
+    def tiles(self):
+        """(ti, tj, payload[count, b, b]) in column-major tile order."""
+        n, b, N, s = self._info()
+        ti = np.empty(s, np.int32)
+        tj = np.empty(s, np.int32)
+        pay = np.empty((s, b, b), np.float64)
+        _check(lib.tib_matrix_tiles(self._h, ti.ctypes.data_as(C.POINTER(C.c_int)),
+                                    tj.ctypes.data_as(C.POINTER(C.c_int)),
+                                    pay.ctypes.data_as(C.POINTER(C.c_double))))
+        return ti, tj, pay
+
+    def to_dense(self) -> np.ndarray:
+        """dense_from_tiled (oracle.cpp:24-45), with the reference's n <= 4000 guard."""
+        n, b, N, s = self._info()
+        if n > _ORACLE_LIMIT:
+            raise TileinvError(f"oracle limited to n <= {_ORACLE_LIMIT}, got n = {n}")
+        ti, tj, pay = self.tiles()
+        return _tiles_to_dense(n, b, ti, tj, pay)
+
+
+class Factor:
+    """TiledFactor (storage.hpp:46-51); device resident (L and the phase-1 tiles)."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib.tib_factor_free(h)
+            self._h = None
+
+    def _info(self):
+        n, b, s = C.c_long(), C.c_int(), C.c_long()
+        _check(lib.tib_factor_info(self._h, C.byref(n), C.byref(b), C.byref(s)))
+        return n.value, b.value, s.value
+
+    @property
+    def n(self) -> int:
+        return self._info()[0]
+
+    @property
+    def tile_size(self) -> int:
+        return self._info()[1]
+
+    @property
+    def stored_tiles(self) -> int:
+        return self._info()[2]
+
+    @property
+    def checksum(self) -> int:
+        out = C.c_uint64()
+        _check(lib.tib_factor_checksum(self._h, C.byref(out)))
+        return out.value
+
+    def logdet(self) -> float:
+        out = C.c_double()
+        _check(lib.tib_factor_logdet(self._h, C.byref(out)))
+        return out.value
+
+    def tiles(self, phase: int = 1):
+        """phase 1: L tiles; phase 2: phase-1 tiles (U on the diagonal, W off it)."""
+        n, b, s = self._info()
+        ti = np.empty(s, np.int32)
+        tj = np.empty(s, np.int32)
+        pay = np.empty((s, b, b), np.float64)
+        _check(lib.tib_factor_tiles(self._h, phase, ti.ctypes.data_as(C.POINTER(C.c_int)),
+                                    tj.ctypes.data_as(C.POINTER(C.c_int)),
+                                    pay.ctypes.data_as(C.POINTER(C.c_double))))
+        return ti, tj, pay
+
+
+class SelectedInverseResult:
+    """SelectedInverse (selinv.hpp:61-68) + its request; device resident."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib.tib_sigma_free(h)
+            self._h = None
+
+    def _info(self):
+        n, b, t, g = C.c_long(), C.c_int(), C.c_long(), C.c_int()
+        _check(lib.tib_sigma_info(self._h, C.byref(n), C.byref(b), C.byref(t), C.byref(g)))
+        return n.value, b.value, t.value, g.value
+
+    @property
+    def n(self) -> int:
+        return self._info()[0]
+
+    @property
+    def closure_tiles(self) -> int:
+        return self._info()[2]
+
+    @property
+    def growth_warning(self) -> bool:
+        return bool(self._info()[3])
+
+    @property
+    def checksum(self) -> int:
+        out = C.c_uint64()
+        _check(lib.tib_sigma_checksum(self._h, C.byref(out)))
+        return out.value
+
+    def entries_arrays(self):
+        """extract_entries (selinv.cpp:387-439) as (rows, cols, values) numpy arrays."""
+        cnt = C.c_long()
+        _check(lib.tib_sigma_entries(self._h, C.byref(cnt), None, None, None))
+        rows = np.empty(cnt.value, np.int64)
+        cols = np.empty(cnt.value, np.int64)
+        vals = np.empty(cnt.value, np.float64)
+        _check(lib.tib_sigma_entries(self._h, C.byref(cnt), _lp(rows), _lp(cols),
+                                     vals.ctypes.data_as(C.POINTER(C.c_double))))
+        return rows, cols, vals
+
+    def entries(self):
+        """List of (r, c, value) tuples, like module.cpp:154-161."""
+        rows, cols, vals = self.entries_arrays()
+        return [(int(r), int(c), float(v)) for r, c, v in zip(rows.tolist(), cols.tolist(), vals.tolist())]
+
+    def diagonal(self) -> np.ndarray:
+        """Marginal variances diag(Sigma), written by the phase-2 diagonal kernel."""
+        n = self._info()[0]
+        out = np.empty(n, np.float64)
+        _check(lib.tib_sigma_diagonal(self._h, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def logdet(self) -> float:
+        out = C.c_double()
+        _check(lib.tib_sigma_logdet(self._h, C.byref(out)))
+        return out.value
+
+    def tiles(self):
+        n, b, t, _ = self._info()
+        ti = np.empty(t, np.int32)
+        tj = np.empty(t, np.int32)
+        pay = np.empty((t, b, b), np.float64)
+        _check(lib.tib_sigma_tiles(self._h, ti.ctypes.data_as(C.POINTER(C.c_int)),
+                                   tj.ctypes.data_as(C.POINTER(C.c_int)),
+                                   pay.ctypes.data_as(C.POINTER(C.c_double))))
+        return ti, tj, pay
+
+    def to_dense(self) -> np.ndarray:
+        """result_to_dense (module.cpp:83-107): zeros outside the closure."""
+        n, b, t, _ = self._info()
+        ti, tj, pay = self.tiles()
+        return _tiles_to_dense(n, b, ti, tj, pay)
+
+
+def _tiles_to_dense(n, b, ti, tj, pay) -> np.ndarray:
+    """Symmetric dense expansion of lower tiles (r >= c kept, mirrored)."""
+    out = np.zeros((n, n))
+    for k in range(len(ti)):
+        r0, c0 = int(ti[k]) * b, int(tj[k]) * b
+        nr, nc = max(0, min(b, n - r0)), max(0, min(b, n - c0))
+        if nr == 0 or nc == 0:
+            continue
+        rows = np.broadcast_to(np.arange(nr)[:, None] + r0, (nr, nc))
+        cols = np.broadcast_to(np.arange(nc)[None, :] + c0, (nr, nc))
+        keep = cols <= rows
+        out[rows[keep], cols[keep]] = pay[k][:nr, :nc][keep]
+    il = np.tril_indices(n, -1)
+    out[il[1], il[0]] = out[il]
+    return out
+
+
+def _new_handle() -> C.c_void_p:
+    return C.c_void_p()
+
+
+def generate(n: int, bandwidth: int, thickness: int, density: float, seed: int = 0,
+             tile_size: int = 32) -> Matrix:
+    """generate_arrowhead (matgen.cpp:59-120), bit-exact values."""
+    h = _new_handle()
+    _check(lib.tib_matrix_generate(n, bandwidth, thickness, float(density), seed, tile_size, C.byref(h)))
+    return Matrix(h.value)
+
+
+def from_dense(array, tile_size: int = 32) -> Matrix:
+    a = np.ascontiguousarray(array, dtype=np.float64)
+    if a.ndim != 2 or a.shape[0] != a.shape[1]:
+        raise ValueError("from_dense needs a square 2-D array")
+    h = _new_handle()
+    _check(lib.tib_matrix_from_dense(a.shape[0], tile_size, a.ctypes.data_as(C.POINTER(C.c_double)),
+                                     C.byref(h)))
+    return Matrix(h.value)
+
+
+def from_tiles(n: int, tile_size: int, ti: Sequence[int], tj: Sequence[int], payload) -> Matrix:
+    ti = np.ascontiguousarray(ti, np.int32)
+    tj = np.ascontiguousarray(tj, np.int32)
+    pay = np.ascontiguousarray(payload, np.float64)
+    h = _new_handle()
+    _check(lib.tib_matrix_from_tiles(n, tile_size, len(ti), ti.ctypes.data_as(C.POINTER(C.c_int)),
+                                     tj.ctypes.data_as(C.POINTER(C.c_int)),
+                                     pay.ctypes.data_as(C.POINTER(C.c_double)), C.byref(h)))
+    return Matrix(h.value)
+
+
+def read_matrix_market(path: str, tile_size: int = 32) -> Matrix:
+    try:
+        with open(path, "rb") as f:
+            text = f.read()
+    except OSError:
+        raise TileinvError(f"cannot open {path}") from None
+    h = _new_handle()
+    _check(lib.tib_matrix_read_mm(text, len(text), tile_size, C.byref(h)))
+    return Matrix(h.value)
+
+
+def write_matrix_market(matrix: Matrix, path: str) -> None:
+    size = C.c_size_t(0)
+    _check(lib.tib_matrix_write_mm(matrix._h, None, C.byref(size)))
+    buf = C.create_string_buffer(size.value)
+    _check(lib.tib_matrix_write_mm(matrix._h, buf, C.byref(size)))
+    try:
+        with open(path, "wb") as f:
+            f.write(buf.raw[: size.value])
+    except OSError:
+        raise TileinvError(f"cannot open {path} for writing") from None
+
+
+def factorize(matrix: Matrix, workers: int = 1, device: int = 0) -> Factor:
+    """symbolic_cholesky + factorize (module.cpp:191-197)."""
+    _check_workers(workers)
+    h = _new_handle()
+    _check(lib.tib_factorize(matrix._h, device, C.byref(h)))
+    return Factor(h.value)
+
+
+def selected_inverse(matrix: Matrix, selection="pattern", workers: int = 1,
+                     device: int = 0) -> SelectedInverseResult:
+    """selected_inverse(matrix, request, workers) (module.cpp:199-206)."""
+    preset, rows, cols, ne = _request(selection)
+    _check_workers(workers)
+    h = _new_handle()
+    _check(lib.tib_selected_inverse(matrix._h, preset, _lp(rows), _lp(cols), ne, device, C.byref(h)))
+    return SelectedInverseResult(h.value)
+
+
+def selected_inverse_of_factor(factor: Factor, selection="pattern",
+                               workers: int = 1) -> SelectedInverseResult:
+    """selected_inverse(factor, request, workers) (module.cpp:208-215)."""
+    preset, rows, cols, ne = _request(selection)
+    _check_workers(workers)
+    h = _new_handle()
+    _check(lib.tib_selected_inverse_of_factor(factor._h, preset, _lp(rows), _lp(cols), ne, C.byref(h)))
+    return SelectedInverseResult(h.value)
+
+
+def selected_inverse_batch(matrices: Sequence[Matrix], device: int = 0):
+    """Batched factorize + pattern selected inversion of matrices sharing one
+    tile pattern: returns (logdet[count], diag[count, n])."""
+    count = len(matrices)
+    if count == 0:
+        raise TileinvError("batch needs at least one matrix")
+    n = matrices[0].n
+    handles = (C.c_void_p * count)(*[m._h.value for m in matrices])
+    logdet = np.empty(count, np.float64)
+    diag = np.empty((count, n), np.float64)
+    _check(lib.tib_selected_inverse_batch(handles, count, device,
+                                          logdet.ctypes.data_as(C.POINTER(C.c_double)),
+                                          diag.ctypes.data_as(C.POINTER(C.c_double))))
+    return logdet, diag
+
+
+def factor_pattern(matrix: Matrix):
+    """symbolic_fill of the matrix pattern as a list of (i, j)."""
+    cnt = C.c_long()
+    _check(lib.tib_symbolic_pattern(matrix._h, C.byref(cnt), None, None))
+    ti = np.empty(cnt.value, np.int32)
+    tj = np.empty(cnt.value, np.int32)
+    _check(lib.tib_symbolic_pattern(matrix._h, C.byref(cnt), ti.ctypes.data_as(C.POINTER(C.c_int)),
+                                    tj.ctypes.data_as(C.POINTER(C.c_int))))
+    return list(zip(ti.tolist(), tj.tolist()))
+
+
+def closure_tiles(matrix: Matrix, selection="pattern"):
+    """select_tiles + symbolic_inversion closure as ((i, j) list, growth_warning)."""
+    preset, rows, cols, ne = _request(selection)
+    cnt, g = C.c_long(), C.c_int()
+    _check(lib.tib_symbolic_closure(matrix._h, preset, _lp(rows), _lp(cols), ne, C.byref(cnt), None, None,
+                                    C.byref(g)))
+    ti = np.empty(cnt.value, np.int32)
+    tj = np.empty(cnt.value, np.int32)
+    _check(lib.tib_symbolic_closure(matrix._h, preset, _lp(rows), _lp(cols), ne, C.byref(cnt),
+                                    ti.ctypes.data_as(C.POINTER(C.c_int)),
+                                    tj.ctypes.data_as(C.POINTER(C.c_int)), C.byref(g)))
+    return list(zip(ti.tolist(), tj.tolist())), bool(g.value)
+
+
+def task_flops(matrix: Matrix, selection="pattern"):
+    """Task-model FLOPs (factorize, phase1, phase2) -- SURVEY.md 8(d)."""
+    preset, rows, cols, ne = _request(selection)
+    f, p1, p2 = C.c_double(), C.c_double(), C.c_double()
+    _check(lib.tib_flops(matrix._h, preset, _lp(rows), _lp(cols), ne, C.byref(f), C.byref(p1), C.byref(p2)))
+    return f.value, p1.value, p2.value
+
+
+def bench_resident(matrix: Matrix, reps: int, warmup: int, device: int = 0):
+    """Device-resident timing of the fused sweep: (ms/rep, ms factor, ms phase2, logdet)."""
+    a, b, c, d = C.c_double(), C.c_double(), C.c_double(), C.c_double()
+    _check(lib.tib_bench_resident(matrix._h, device, reps, warmup, C.byref(a), C.byref(b), C.byref(c),
+                                  C.byref(d)))
+    return a.value, b.value, c.value, d.value
+
+
+def device_count() -> int:
+    c = C.c_int()
+    _check(lib.tib_device_count(C.byref(c)))
+    return c.value
+
+
+__all__ = [
+    "Factor", "Matrix", "NotSpdError", "SelectedInverseResult", "TileinvError", "__version__",
+    "factorize", "from_dense", "from_tiles", "generate", "read_matrix_market", "selected_inverse",
+    "selected_inverse_of_factor", "write_matrix_market", "selected_inverse_batch", "factor_pattern",
+    "closure_tiles", "task_flops", "bench_resident", "device_count",
+]

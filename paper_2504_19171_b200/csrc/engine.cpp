@@ -1,0 +1,1177 @@
+// Host engine of the B200 path: builds pointer-free task plans from the
+// symbolic planner, owns device stores, runs the two column sweeps on a CUDA
+// stream (captured once into a CUDA graph per plan), and implements the C ABI
+// declared in include/tileinv_b200.h.
+//
+// Device data layout: every store is one contiguous
+// allocation of `tiles x bp x bp` doubles in pattern slot order (column-major
+// over the tile grid, diagonal first in each column), bp = b rounded up to 64
+// with identity padding on diagonal tiles.  Stores: A (working copy, Schur
+// updates in place), L (factor), P1 (X_j = L_jj^{-1} on diagonal slots,
+// W_kj = L_kj X_j off them), Sigma (closure slots), Var (N x bp marginal
+// variances), Scratch, Logdet (N x bp/64 partial sums).
+//
+// Column sweep (fused factorization + phase 1), per column j, in order:
+//   diag_cluster_kernel : L_jj = chol(A_jj), X_j = L_jj^{-1}         (potrf_tile + trtri_tile)
+//   gemm tasks          : L_kj = A_kj X_j^T  for k in nb(j), k > j     (trsm_tile recast)
+//   gemm tasks          : W_kj = L_kj X_j                               (trmm_tile, phase 1)
+//                         A_ab -= L_aj L_bj^T, a >= b in nb(j) > j      (syrk_tile / gemm_tile)
+// Phase-2 sweep, per closure column i descending (selinv.cpp:239-345):
+//   gemm tasks          : Sigma_ji = -sum_k M_jk W_ki                   (gemm_tile, off-diagonal)
+//   gemm tasks          : Sigma_ii = X_i^T X_i - sum_k W_ki^T Sigma_ki  (lauum_tile + gemm_tile),
+//                         mirrored exactly, diag -> Var
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/tileinv_b200.h"
+#include "kernels.cuh"
+#include "planner.hpp"
+
+namespace tib {
+
+#define CK(x)                                                                                   \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess) throw Error(kErrCuda, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+static constexpr int kBlk = 64;
+static int padded_b(int b) { return (b + kBlk - 1) / kBlk * kBlk; }
+
+// ---------------------------------------------------------------------------
+// memory
+struct DevBuf {
+  double* p = nullptr;
+  size_t n = 0;  // doubles
+  int dev = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(size_t doubles, int device, cudaStream_t stream) : n(doubles), dev(device), s(stream) {
+    if (n) CK(cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(double), s));
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), dev(o.dev), s(o.s) {
+    o.p = nullptr;
+    o.n = 0;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      n = o.n;
+      dev = o.dev;
+      s = o.s;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
+  // stream-ordered free back into the device pool (release threshold = max)
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { release(); }
+};
+
+template <class T>
+struct DevArray {
+  T* p = nullptr;
+  size_t n = 0;
+  void upload(const std::vector<T>& v, cudaStream_t s) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = v.size();
+    if (n) {
+      CK(cudaMalloc(reinterpret_cast<void**>(&p), n * sizeof(T)));
+      CK(cudaMemcpyAsync(p, v.data(), n * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+  }
+  ~DevArray() {
+    if (p) cudaFree(p);
+  }
+};
+
+// Pinned host staging (falls back to pageable memory without a device).
+struct HostBuf {
+  double* p = nullptr;
+  size_t n = 0;
+  bool pinned = false;
+  HostBuf() = default;
+  explicit HostBuf(size_t doubles) { alloc(doubles); }
+  void alloc(size_t doubles) {
+    free_();
+    n = doubles;
+    if (!n) return;
+    if (cudaMallocHost(reinterpret_cast<void**>(&p), n * sizeof(double)) == cudaSuccess) {
+      pinned = true;
+    } else {
+      cudaGetLastError();
+      p = static_cast<double*>(std::malloc(n * sizeof(double)));
+      if (!p) throw Error(kErrGeneric, "host allocation failed");
+      pinned = false;
+    }
+  }
+  void free_() {
+    if (p) {
+      if (pinned) cudaFreeHost(p);
+      else std::free(p);
+    }
+    p = nullptr;
+    n = 0;
+  }
+  HostBuf(const HostBuf&) = delete;
+  HostBuf& operator=(const HostBuf&) = delete;
+  HostBuf(HostBuf&& o) noexcept : p(o.p), n(o.n), pinned(o.pinned) {
+    o.p = nullptr;
+    o.n = 0;
+  }
+  HostBuf& operator=(HostBuf&& o) noexcept {
+    if (this != &o) {
+      free_();
+      p = o.p;
+      n = o.n;
+      pinned = o.pinned;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
+  ~HostBuf() { free_(); }
+};
+
+// ---------------------------------------------------------------------------
+// per-device runtime
+struct DeviceRt {
+  int dev = -1;
+  cudaStream_t stream = nullptr;
+  bool ready = false;
+};
+static std::mutex g_rt_mu;
+static DeviceRt g_rt[16];
+
+static DeviceRt& runtime(int device) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    throw Error(kErrCuda, "no CUDA device available (the B200 path has no CPU fallback)");
+  }
+  if (device < 0 || device >= count || device >= 16)
+    throw Error(kErrInvalidArgument, "device index " + std::to_string(device) + " out of range");
+  std::lock_guard<std::mutex> lk(g_rt_mu);
+  DeviceRt& rt = g_rt[device];
+  CK(cudaSetDevice(device));
+  if (!rt.ready) {
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thresh = UINT64_MAX;
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+    CK(cudaStreamCreateWithFlags(&rt.stream, cudaStreamNonBlocking));
+    CK(static_cast<cudaError_t>(configure_kernels()));
+    rt.dev = device;
+    rt.ready = true;
+  }
+  return rt;
+}
+
+// ---------------------------------------------------------------------------
+// plans
+struct Launch {
+  int begin = 0, count = 0;
+};
+
+static long long tile_off(long slot, int bp) { return static_cast<long long>(slot) * bp * bp; }
+static long long blk_off(long slot, int bp, int p, int q) {
+  return tile_off(slot, bp) + static_cast<long long>(p) * kBlk * bp + static_cast<long long>(q) * kBlk;
+}
+
+static Task make_task(unsigned char c_store, long long c_off, int bp, int m0, int n0, int seg_begin,
+                      int seg_count) {
+  Task t{};
+  t.c_store = c_store;
+  t.c_off = c_off;
+  t.c0_store = kStoreNone;
+  t.cm_store = kStoreNone;
+  t.diag_store = kStoreNone;
+  t.ldc = t.ldc0 = bp;
+  t.m0 = m0;
+  t.n0 = n0;
+  t.seg_begin = seg_begin;
+  t.seg_count = seg_count;
+  t.mode = kFull;
+  return t;
+}
+static Seg make_seg(unsigned char as, long long ao, unsigned char bs, long long bo, int bp, int klo, int khi,
+                    int flags) {
+  Seg s{};
+  s.a_store = as;
+  s.a_off = ao;
+  s.b_store = bs;
+  s.b_off = bo;
+  s.lda = s.ldb = bp;
+  s.k_lo = static_cast<short>(klo);
+  s.k_hi = static_cast<short>(khi);
+  s.flags = static_cast<unsigned char>(flags);
+  return s;
+}
+
+// Graph of one sweep for a given batch size (the base tables it reads live in
+// device memory, so the graph never depends on store addresses).
+struct GraphCache {
+  struct Entry {
+    cudaGraphExec_t exec = nullptr;
+    BaseTable* tables = nullptr;  // device copy of the per-matrix base tables, owned here
+  };
+  std::map<int, Entry> by_batch;
+  Entry& get(int batch) {
+    Entry& e = by_batch[batch];
+    if (!e.tables) CK(cudaMalloc(reinterpret_cast<void**>(&e.tables), sizeof(BaseTable) * batch));
+    return e;
+  }
+  ~GraphCache() {
+    for (auto& kv : by_batch) {
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+      if (kv.second.tables) cudaFree(kv.second.tables);
+    }
+  }
+};
+
+struct FactorPlan2 {
+  Layout L;
+  int bp = 0, nb = 0, cluster = 1;
+  FactorPlan sym;  // filled pattern + counts
+  std::vector<Task> tasks;
+  std::vector<Seg> segs;
+  std::vector<DiagJob> jobs;
+  struct Col {
+    Launch panel, wupd;
+  };
+  std::vector<Col> cols;
+  int device = -1;
+  DevArray<Task> d_tasks;
+  DevArray<Seg> d_segs;
+  DevArray<DiagJob> d_jobs;
+  GraphCache graphs;
+  std::mutex mu;
+};
+
+struct Phase2Plan {
+  Layout L;
+  int bp = 0, nb = 0;
+  Closure sel;
+  std::vector<Task> tasks;
+  std::vector<Seg> segs;
+  struct Col {
+    Launch off, diag;
+  };
+  std::vector<Col> cols;
+  int device = -1;
+  DevArray<Task> d_tasks;
+  DevArray<Seg> d_segs;
+  GraphCache graphs;
+  std::mutex mu;
+};
+
+static std::shared_ptr<FactorPlan2> build_factor_plan(const Pattern& pattern) {
+  auto plan = std::make_shared<FactorPlan2>();
+  plan->sym = symbolic_cholesky(pattern);
+  const Pattern& F = plan->sym.filled;
+  const Layout& L = F.layout();
+  plan->L = L;
+  const int bp = padded_b(L.b), nb = bp / kBlk;
+  plan->bp = bp;
+  plan->nb = nb;
+  plan->cluster = nb >= 8 ? 16 : nb >= 4 ? 8 : nb >= 2 ? 4 : 1;
+  auto& T = plan->tasks;
+  auto& S = plan->segs;
+  for (int j = 0; j < L.N; ++j) {
+    const long dslot = F.col_start(j);
+    DiagJob job{};
+    job.a_off = job.l_off = job.x_off = tile_off(dslot, bp);
+    job.t_off = 0;
+    job.logdet_off = static_cast<long long>(j) * nb;
+    job.pivot_base = static_cast<long long>(j) * L.b;
+    job.valid_rows = static_cast<int>(std::min<long>(L.b, L.n - static_cast<long>(j) * L.b));
+    job.mode = kFactorInvert;
+    plan->jobs.push_back(job);
+    FactorPlan2::Col col;
+    std::vector<long> ks;  // slots of rows > j
+    std::vector<int> krows;
+    for (const int* r = F.rows_begin(j); r != F.rows_end(j); ++r)
+      if (*r > j) {
+        krows.push_back(*r);
+        ks.push_back(F.slot(*r, j));
+      }
+    // L_kj = A_kj X_j^T (X^T upper: k < n0 + 64)
+    col.panel.begin = static_cast<int>(T.size());
+    for (long sk : ks)
+      for (int p = 0; p < nb; ++p)
+        for (int q = 0; q < nb; ++q) {
+          T.push_back(make_task(kStoreL, blk_off(sk, bp, p, q), bp, p * kBlk, q * kBlk, static_cast<int>(S.size()), 1));
+          S.push_back(make_seg(kStoreA, tile_off(sk, bp), kStoreP1, tile_off(dslot, bp), bp, 0, (q + 1) * kBlk, kTransB));
+        }
+    col.panel.count = static_cast<int>(T.size()) - col.panel.begin;
+    col.wupd.begin = static_cast<int>(T.size());
+    // window update first (it feeds the next diagonal), then W
+    for (size_t ib = 0; ib < krows.size(); ++ib)
+      for (size_t ia = ib; ia < krows.size(); ++ia) {
+        const int a = krows[ia], c = krows[ib];
+        const long ts = F.slot(a, c);
+        if (ts < 0) throw Error(kErrConsistency, "update target outside the filled pattern");
+        for (int p = 0; p < nb; ++p)
+          for (int q = 0; q < (a == c ? p + 1 : nb); ++q) {
+            Task t = make_task(kStoreA, blk_off(ts, bp, p, q), bp, p * kBlk, q * kBlk, static_cast<int>(S.size()), 1);
+            t.c0_store = kStoreA;
+            t.c0_off = t.c_off;
+            T.push_back(t);
+            S.push_back(make_seg(kStoreL, tile_off(ks[ia], bp), kStoreL, tile_off(ks[ib], bp), bp, 0, bp,
+                                 kTransB | kNegate));
+          }
+      }
+    // W_kj = L_kj X_j (X lower: k >= n0)
+    for (long sk : ks)
+      for (int p = 0; p < nb; ++p)
+        for (int q = 0; q < nb; ++q) {
+          T.push_back(make_task(kStoreP1, blk_off(sk, bp, p, q), bp, p * kBlk, q * kBlk, static_cast<int>(S.size()), 1));
+          S.push_back(make_seg(kStoreL, tile_off(sk, bp), kStoreP1, tile_off(dslot, bp), bp, q * kBlk, bp, 0));
+        }
+    col.wupd.count = static_cast<int>(T.size()) - col.wupd.begin;
+    plan->cols.push_back(col);
+  }
+  return plan;
+}
+
+static std::shared_ptr<Phase2Plan> build_phase2_plan(const Pattern& F, const Closure& sel) {
+  auto plan = std::make_shared<Phase2Plan>();
+  const Layout& L = F.layout();
+  plan->L = L;
+  plan->sel = sel;
+  const Pattern& C = plan->sel.closure;
+  const int bp = padded_b(L.b), nb = bp / kBlk;
+  plan->bp = bp;
+  plan->nb = nb;
+  auto& T = plan->tasks;
+  auto& S = plan->segs;
+  auto cslot = [&](int i, int j) {
+    const long s = C.slot(i, j);
+    if (s < 0)
+      throw Error(kErrConsistency, "operand tile (" + std::to_string(i) + ", " + std::to_string(j) +
+                                       ") missing from the closure");
+    return s;
+  };
+  for (const ColumnWork& cw : plan->sel.columns) {
+    const int i = cw.col;
+    std::vector<int> ks;
+    for (const int* r = F.rows_begin(i); r != F.rows_end(i); ++r)
+      if (*r > i) ks.push_back(*r);
+    Phase2Plan::Col col;
+    col.off.begin = static_cast<int>(T.size());
+    for (int j : cw.offdiag_rows) {
+      const long ts = cslot(j, i);
+      for (int p = 0; p < nb; ++p)
+        for (int q = 0; q < nb; ++q) {
+          T.push_back(make_task(kStoreSigma, blk_off(ts, bp, p, q), bp, p * kBlk, q * kBlk, static_cast<int>(S.size()),
+                                static_cast<int>(ks.size())));
+          for (int k : ks) {
+            const long ms = cslot(std::max(j, k), std::min(j, k));
+            S.push_back(make_seg(kStoreSigma, tile_off(ms, bp), kStoreP1, tile_off(F.slot(k, i), bp), bp, 0, bp,
+                                 (k > j ? kTransA : 0) | kNegate));
+          }
+        }
+    }
+    col.off.count = static_cast<int>(T.size()) - col.off.begin;
+    col.diag.begin = static_cast<int>(T.size());
+    if (cw.diagonal) {
+      const long ds = cslot(i, i);
+      const long xs = F.slot(i, i);
+      for (int p = 0; p < nb; ++p)
+        for (int q = 0; q <= p; ++q) {
+          Task t = make_task(kStoreSigma, blk_off(ds, bp, p, q), bp, p * kBlk, q * kBlk, static_cast<int>(S.size()),
+                             1 + static_cast<int>(ks.size()));
+          if (p == q) {
+            t.mode = kSymDiag;
+            t.diag_store = kStoreVar;
+            t.diag_off = static_cast<long long>(i) * bp + p * kBlk;
+          } else {
+            t.mode = kMirror;
+            t.cm_store = kStoreSigma;
+            t.cm_off = blk_off(ds, bp, q, p);
+          }
+          T.push_back(t);
+          // U U^T = X^T X; rows >= p*64 of X are the only nonzero contributions
+          S.push_back(make_seg(kStoreP1, tile_off(xs, bp), kStoreP1, tile_off(xs, bp), bp, p * kBlk, bp, kTransA));
+          for (int k : ks)
+            S.push_back(make_seg(kStoreP1, tile_off(F.slot(k, i), bp), kStoreSigma, tile_off(cslot(k, i), bp), bp, 0, bp,
+                                 kTransA | kNegate));
+        }
+    }
+    col.diag.count = static_cast<int>(T.size()) - col.diag.begin;
+    plan->cols.push_back(col);
+  }
+  return plan;
+}
+
+// plan caches (keyed by layout + pattern tiles [+ closure tiles])
+static uint64_t pattern_hash(const Pattern& p, uint64_t seed) {
+  Fnv h;
+  h.h ^= seed;
+  const Layout& L = p.layout();
+  h.mix(&L.n, sizeof(L.n));
+  h.mix(&L.b, sizeof(L.b));
+  for (const Coord& c : p.tiles()) h.mix(&c, sizeof(c));
+  return h.h;
+}
+static std::mutex g_plan_mu;
+static std::map<std::pair<int, uint64_t>, std::shared_ptr<FactorPlan2>> g_fplans;
+static std::map<std::pair<int, uint64_t>, std::shared_ptr<Phase2Plan>> g_p2plans;
+
+static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int device, cudaStream_t s) {
+  const uint64_t key = pattern_hash(pattern, 1);
+  {
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    auto it = g_fplans.find({device, key});
+    if (it != g_fplans.end() && it->second->L.n == pattern.layout().n) return it->second;
+  }
+  auto plan = build_factor_plan(pattern);
+  plan->device = device;
+  plan->d_tasks.upload(plan->tasks, s);
+  plan->d_segs.upload(plan->segs, s);
+  plan->d_jobs.upload(plan->jobs, s);
+  CK(cudaStreamSynchronize(s));
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  if (g_fplans.size() > 8) g_fplans.clear();
+  g_fplans[{device, key}] = plan;
+  return plan;
+}
+
+static std::shared_ptr<Phase2Plan> phase2_plan_for(const Pattern& F, const Closure& sel, int device,
+                                                   cudaStream_t s) {
+  const uint64_t key = pattern_hash(sel.closure, pattern_hash(F, 2));
+  {
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    auto it = g_p2plans.find({device, key});
+    if (it != g_p2plans.end()) return it->second;
+  }
+  auto plan = build_phase2_plan(F, sel);
+  plan->device = device;
+  plan->d_tasks.upload(plan->tasks, s);
+  plan->d_segs.upload(plan->segs, s);
+  CK(cudaStreamSynchronize(s));
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  if (g_p2plans.size() > 16) g_p2plans.clear();
+  g_p2plans[{device, key}] = plan;
+  return plan;
+}
+
+// ---------------------------------------------------------------------------
+// sweeps
+static bool use_graphs() {
+  const char* e = std::getenv("TIB_GRAPH");
+  return !(e && e[0] == '0');
+}
+
+static void enqueue_factor_sweep(FactorPlan2& P, const BaseTable* d_tables, int batch, cudaStream_t s) {
+  for (int j = 0; j < P.L.N; ++j) {
+    launch_diag_jobs(P.d_jobs.p + j, 1, d_tables, batch, P.bp, P.cluster, s);
+    const auto& c = P.cols[static_cast<size_t>(j)];
+    launch_gemm_tasks(P.d_tasks.p + c.panel.begin, P.d_segs.p, c.panel.count, d_tables, batch, s);
+    launch_gemm_tasks(P.d_tasks.p + c.wupd.begin, P.d_segs.p, c.wupd.count, d_tables, batch, s);
+  }
+}
+
+static void enqueue_phase2_sweep(Phase2Plan& P, const BaseTable* d_tables, int batch, cudaStream_t s) {
+  for (const auto& c : P.cols) {
+    launch_gemm_tasks(P.d_tasks.p + c.off.begin, P.d_segs.p, c.off.count, d_tables, batch, s);
+    launch_gemm_tasks(P.d_tasks.p + c.diag.begin, P.d_segs.p, c.diag.count, d_tables, batch, s);
+  }
+}
+
+// Uploads the base tables into the plan-owned buffer and runs the sweep,
+// replaying a CUDA graph captured on first use for this batch size.  The
+// graph's only baked-in pointers are plan-owned (tasks, segs, jobs, tables).
+template <class Plan, class Enq>
+static void run_graph(Plan& P, const std::vector<BaseTable>& tables, cudaStream_t s, Enq&& enqueue) {
+  const int batch = static_cast<int>(tables.size());
+  GraphCache::Entry& e = P.graphs.get(batch);
+  CK(cudaMemcpyAsync(e.tables, tables.data(), sizeof(BaseTable) * batch, cudaMemcpyHostToDevice, s));
+  if (!use_graphs()) {
+    enqueue(e.tables);
+    CK(cudaGetLastError());
+    return;
+  }
+  if (!e.exec) {
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    enqueue(e.tables);
+    const cudaError_t le = cudaGetLastError();
+    CK(cudaStreamEndCapture(s, &g));
+    CK(le);
+    CK(cudaGraphInstantiate(&e.exec, g, 0));
+    cudaGraphDestroy(g);
+  }
+  CK(cudaGraphLaunch(e.exec, s));
+}
+
+// ---------------------------------------------------------------------------
+// objects behind the handles
+struct MatrixObj {
+  Layout layout;
+  Pattern pattern;
+  HostBuf payload;  // pattern.size() * b * b, pinned when a device exists
+};
+
+struct FactorObj {
+  int device = 0;
+  Layout layout;
+  std::shared_ptr<FactorPlan2> plan;
+  DevBuf L, P1;
+  double logdet = 0;
+};
+
+struct SigmaObj {
+  int device = 0;
+  Layout layout;
+  Request req;
+  std::shared_ptr<Phase2Plan> plan;
+  DevBuf S, var;
+  double logdet = 0;
+  std::unique_ptr<HostBuf> host;  // lazily downloaded bp-layout tiles
+};
+
+static void fill_matrix(MatrixObj& m, HostMatrix&& hm) {
+  m.layout = hm.layout;
+  m.pattern = std::move(hm.pattern);
+  m.payload.alloc(hm.payload.size());
+  std::memcpy(m.payload.p, hm.payload.data(), hm.payload.size() * sizeof(double));
+}
+
+// Host matrix -> bp-layout A store over the FILLED pattern (fill-in tiles zero,
+// identity on the padded diagonal).
+static void upload_matrix(const MatrixObj& m, const Pattern& filled, int bp, double* dA, cudaStream_t s,
+                          HostBuf* staging_keep = nullptr) {
+  const int b = m.layout.b;
+  const size_t bb = static_cast<size_t>(b) * b, bpp = static_cast<size_t>(bp) * bp;
+  if (bp == b && filled == m.pattern) {
+    CK(cudaMemcpyAsync(dA, m.payload.p, filled.size() * bb * sizeof(double), cudaMemcpyHostToDevice, s));
+    return;
+  }
+  HostBuf local;
+  HostBuf& st = staging_keep ? *staging_keep : local;
+  st.alloc(filled.size() * bpp);
+  std::memset(st.p, 0, st.n * sizeof(double));
+  for (size_t k = 0; k < filled.size(); ++k) {
+    const Coord& c = filled.tiles()[k];
+    double* dst = st.p + k * bpp;
+    const long src = m.pattern.slot(c.i, c.j);
+    if (src >= 0)
+      for (int r = 0; r < b; ++r)
+        std::memcpy(dst + static_cast<size_t>(r) * bp, m.payload.p + static_cast<size_t>(src) * bb + static_cast<size_t>(r) * b,
+                    b * sizeof(double));
+    if (c.i == c.j)
+      for (int r = b; r < bp; ++r) dst[static_cast<size_t>(r) * bp + r] = 1.0;
+  }
+  CK(cudaMemcpyAsync(dA, st.p, st.n * sizeof(double), cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
+}
+
+struct SweepStores {
+  DevBuf A, L, P1, scratch, logdet;
+  DevBuf status;  // DevStatus per matrix (as doubles storage)
+};
+
+static void alloc_factor_stores(SweepStores& st, const FactorPlan2& P, int batch, int dev, cudaStream_t s) {
+  const size_t tile = static_cast<size_t>(P.bp) * P.bp;
+  const size_t T = P.sym.filled.size();
+  st.A = DevBuf(T * tile * batch, dev, s);
+  st.L = DevBuf(T * tile * batch, dev, s);
+  st.P1 = DevBuf(T * tile * batch, dev, s);
+  st.scratch = DevBuf(tile * batch, dev, s);
+  st.logdet = DevBuf(static_cast<size_t>(P.L.N) * P.nb * batch, dev, s);
+  st.status = DevBuf(static_cast<size_t>(batch), dev, s);
+}
+
+static void check_status(const DevBuf& status, int batch, const Layout& L, cudaStream_t s, int* bad_index = nullptr) {
+  std::vector<unsigned long long> h(static_cast<size_t>(batch));
+  CK(cudaMemcpyAsync(h.data(), status.p, batch * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (int k = 0; k < batch; ++k)
+    if (h[static_cast<size_t>(k)] != ULLONG_MAX) {
+      const long pivot = static_cast<long>(h[static_cast<size_t>(k)]);
+      const int tile = static_cast<int>(pivot / L.b);
+      if (bad_index) *bad_index = k;
+      throw NotSpd("matrix is not positive definite", pivot, tile, tile);
+    }
+}
+
+static double reduce_logdet(const double* parts, int N, int nb) {
+  double s = 0.0;
+  for (int j = 0; j < N; ++j)
+    for (int k = 0; k < nb; ++k) s += parts[static_cast<size_t>(j) * nb + k];
+  return 2.0 * s;
+}
+
+// Runs the fused factor sweep for the matrices already resident in their A stores.
+static void factor_sweep(FactorPlan2& P, SweepStores& st, cudaStream_t s, const std::vector<BaseTable>& tables) {
+  CK(cudaMemsetAsync(st.status.p, 0xff, tables.size() * sizeof(unsigned long long), s));
+  std::lock_guard<std::mutex> lk(P.mu);
+  run_graph(P, tables, s, [&](const BaseTable* d_tables) {
+    enqueue_factor_sweep(P, d_tables, static_cast<int>(tables.size()), s);
+  });
+}
+
+static void phase2_sweep(Phase2Plan& P, cudaStream_t s, const std::vector<BaseTable>& tables) {
+  std::lock_guard<std::mutex> lk(P.mu);
+  run_graph(P, tables, s, [&](const BaseTable* d_tables) {
+    enqueue_phase2_sweep(P, d_tables, static_cast<int>(tables.size()), s);
+  });
+}
+
+static BaseTable make_table(double* A, double* L, double* P1, double* Sg, double* var, double* scratch,
+                            double* logdet, double* status = nullptr) {
+  BaseTable t{};
+  t.p[kStoreA] = A;
+  t.p[kStoreL] = L;
+  t.p[kStoreP1] = P1;
+  t.p[kStoreSigma] = Sg;
+  t.p[kStoreVar] = var;
+  t.p[kStoreScratch] = scratch;
+  t.p[kStoreLogdet] = logdet;
+  t.p[kStoreStatus] = status;
+  return t;
+}
+
+static Request make_request(int preset, const long* rows, const long* cols, long n) {
+  Request r;
+  r.preset = preset;
+  if (preset == kNone) {
+    if (n < 0 || (n > 0 && (!rows || !cols))) throw Error(kErrInvalidArgument, "entry list pointers are null");
+    r.entries.reserve(static_cast<size_t>(n));
+    for (long k = 0; k < n; ++k) r.entries.push_back({rows[k], cols[k]});
+  } else if (preset < 0 || preset > 3) {
+    throw Error(kErrInvalidArgument, "unknown selection preset " + std::to_string(preset));
+  }
+  return r;
+}
+
+// fused factorize + phase 2 for one matrix; returns the result object
+static SigmaObj* selected_inverse_matrix(const MatrixObj& m, const Request& req, int device) {
+  DeviceRt& rt = runtime(device);
+  cudaStream_t s = rt.stream;
+  auto fp = factor_plan_for(m.pattern, device, s);
+  const Pattern& F = fp->sym.filled;
+  const Closure sel = symbolic_inversion(select_tiles(F.layout(), F, req), F);
+  auto p2 = phase2_plan_for(F, sel, device, s);
+  SweepStores st;
+  alloc_factor_stores(st, *fp, 1, device, s);
+  upload_matrix(m, F, fp->bp, st.A.p, s);
+  auto* res = new SigmaObj;
+  std::unique_ptr<SigmaObj> guard(res);
+  res->device = device;
+  res->layout = m.layout;
+  res->req = req;
+  res->plan = p2;
+  const size_t tile = static_cast<size_t>(fp->bp) * fp->bp;
+  res->S = DevBuf(p2->sel.closure.size() * tile, device, s);
+  res->var = DevBuf(static_cast<size_t>(m.layout.N) * fp->bp, device, s);
+  std::vector<BaseTable> tables{make_table(st.A.p, st.L.p, st.P1.p, res->S.p, res->var.p, st.scratch.p, st.logdet.p, st.status.p)};
+  factor_sweep(*fp, st, s, tables);
+  phase2_sweep(*p2, s, tables);
+  std::vector<double> parts(static_cast<size_t>(m.layout.N) * fp->nb);
+  CK(cudaMemcpyAsync(parts.data(), st.logdet.p, parts.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  check_status(st.status, 1, m.layout, s);
+  res->logdet = reduce_logdet(parts.data(), m.layout.N, fp->nb);
+  return guard.release();
+}
+
+static void download_tiles(const DevBuf& store, const Pattern& pat, int b, int bp, int* ti, int* tj, double* payload,
+                           cudaStream_t s, bool transpose_diag) {
+  const size_t bb = static_cast<size_t>(b) * b, bpp = static_cast<size_t>(bp) * bp;
+  HostBuf h(pat.size() * bpp);
+  CK(cudaMemcpyAsync(h.p, store.p, h.n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (size_t k = 0; k < pat.size(); ++k) {
+    const Coord& c = pat.tiles()[k];
+    if (ti) ti[k] = c.i;
+    if (tj) tj[k] = c.j;
+    if (!payload) continue;
+    double* dst = payload + k * bb;
+    const double* src = h.p + k * bpp;
+    if (transpose_diag && c.i == c.j) {
+      for (int r = 0; r < b; ++r)
+        for (int q = 0; q < b; ++q) dst[static_cast<size_t>(r) * b + q] = src[static_cast<size_t>(q) * bp + r];
+    } else {
+      for (int r = 0; r < b; ++r) std::memcpy(dst + static_cast<size_t>(r) * b, src + static_cast<size_t>(r) * bp, b * sizeof(double));
+    }
+  }
+}
+
+static const double* sigma_host(SigmaObj& sg) {
+  if (!sg.host) {
+    DeviceRt& rt = runtime(sg.device);
+    auto h = std::make_unique<HostBuf>(sg.S.n);
+    CK(cudaMemcpyAsync(h->p, sg.S.p, h->n * sizeof(double), cudaMemcpyDeviceToHost, rt.stream));
+    CK(cudaStreamSynchronize(rt.stream));
+    sg.host = std::move(h);
+  }
+  return sg.host->p;
+}
+
+static uint64_t checksum_store(const double* hostbp, const Pattern& pat, int b, int bp) {
+  Fnv h;
+  const size_t bpp = static_cast<size_t>(bp) * bp;
+  for (size_t k = 0; k < pat.size(); ++k) {
+    const Coord& c = pat.tiles()[k];
+    const uint64_t key = tile_key(c.i, c.j);
+    h.mix(&key, sizeof(key));
+    const double* src = hostbp + k * bpp;
+    for (int r = 0; r < b; ++r) h.mix(src + static_cast<size_t>(r) * bp, b * sizeof(double));
+  }
+  return h.h;
+}
+
+// ---------------------------------------------------------------------------
+// error plumbing
+static thread_local std::string t_err;
+static thread_local long t_pivot = -1;
+static thread_local int t_ti = -1, t_tj = -1;
+
+template <class F>
+static int guarded(F&& f) {
+  try {
+    f();
+    return kOk;
+  } catch (const NotSpd& e) {
+    t_err = e.what();
+    t_pivot = e.pivot;
+    t_ti = e.tile_i;
+    t_tj = e.tile_j;
+    return kErrNotSpd;
+  } catch (const Error& e) {
+    t_err = e.what();
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    t_err = "out of host memory";
+    return kErrGeneric;
+  } catch (const std::exception& e) {
+    t_err = e.what();
+    return kErrGeneric;
+  }
+}
+
+template <class T>
+static T* need(T* p, const char* what) {
+  if (!p) throw Error(kErrInvalidArgument, std::string("null ") + what + " handle");
+  return p;
+}
+
+}  // namespace tib
+
+using namespace tib;
+
+struct tib_matrix_s : MatrixObj {};
+struct tib_factor_s : FactorObj {};
+struct tib_sigma_s : SigmaObj {};
+
+extern "C" {
+
+const char* tib_version(void) { return "0.1.0"; }
+const char* tib_last_error_message(void) { return t_err.c_str(); }
+int tib_last_not_spd(long* pivot, int* ti, int* tj) {
+  if (pivot) *pivot = t_pivot;
+  if (ti) *ti = t_ti;
+  if (tj) *tj = t_tj;
+  return kOk;
+}
+int tib_device_count(int* count) {
+  return guarded([&] {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+      cudaGetLastError();
+      c = 0;
+    }
+    *count = c;
+  });
+}
+
+static tib_matrix wrap(HostMatrix&& hm) {
+  auto* out = new tib_matrix_s;
+  fill_matrix(*out, std::move(hm));
+  return out;
+}
+
+int tib_matrix_generate(long n, long w, long t, double density, uint64_t seed, int b, tib_matrix* out) {
+  return guarded([&] { *out = wrap(generate_arrowhead(n, w, t, density, seed, b)); });
+}
+int tib_matrix_from_dense(long n, int b, const double* a, tib_matrix* out) {
+  return guarded([&] {
+    if (n < 1 || !a) throw Error(kErrInvalidArgument, "from_dense needs a square 2-D array");
+    *out = wrap(matrix_from_dense(n, b, a));
+  });
+}
+int tib_matrix_from_tiles(long n, int b, long count, const int* ti, const int* tj, const double* payload,
+                          tib_matrix* out) {
+  return guarded([&] { *out = wrap(matrix_from_tiles(n, b, count, ti, tj, payload)); });
+}
+int tib_matrix_read_mm(const char* text, size_t len, int b, tib_matrix* out) {
+  return guarded([&] { *out = wrap(read_matrix_market(std::string(text, len), b)); });
+}
+int tib_matrix_write_mm(tib_matrix m, char* buf, size_t* len) {
+  return guarded([&] {
+    need(m, "matrix");
+    HostMatrix hm;
+    hm.layout = m->layout;
+    hm.pattern = m->pattern;
+    hm.payload.assign(m->payload.p, m->payload.p + m->payload.n);
+    const std::string text = write_matrix_market(hm);
+    if (buf && *len >= text.size()) std::memcpy(buf, text.data(), text.size());
+    *len = text.size();
+  });
+}
+int tib_matrix_info(tib_matrix m, long* n, int* b, int* N, long* stored) {
+  return guarded([&] {
+    need(m, "matrix");
+    if (n) *n = m->layout.n;
+    if (b) *b = m->layout.b;
+    if (N) *N = m->layout.N;
+    if (stored) *stored = static_cast<long>(m->pattern.size());
+  });
+}
+int tib_matrix_tiles(tib_matrix m, int* ti, int* tj, double* payload) {
+  return guarded([&] {
+    need(m, "matrix");
+    for (size_t k = 0; k < m->pattern.size(); ++k) {
+      if (ti) ti[k] = m->pattern.tiles()[k].i;
+      if (tj) tj[k] = m->pattern.tiles()[k].j;
+    }
+    if (payload) std::memcpy(payload, m->payload.p, m->payload.n * sizeof(double));
+  });
+}
+int tib_matrix_free(tib_matrix m) {
+  delete m;
+  return kOk;
+}
+
+int tib_symbolic_pattern(tib_matrix m, long* count, int* ti, int* tj) {
+  return guarded([&] {
+    need(m, "matrix");
+    const Pattern F = symbolic_fill(m->pattern);
+    *count = static_cast<long>(F.size());
+    if (ti && tj)
+      for (size_t k = 0; k < F.size(); ++k) {
+        ti[k] = F.tiles()[k].i;
+        tj[k] = F.tiles()[k].j;
+      }
+  });
+}
+int tib_symbolic_closure(tib_matrix m, int preset, const long* rows, const long* cols, long ne, long* count,
+                         int* ti, int* tj, int* growth) {
+  return guarded([&] {
+    need(m, "matrix");
+    const Pattern F = symbolic_fill(m->pattern);
+    const Closure c = symbolic_inversion(select_tiles(F.layout(), F, make_request(preset, rows, cols, ne)), F);
+    *count = static_cast<long>(c.closure.size());
+    if (growth) *growth = c.growth_warning ? 1 : 0;
+    if (ti && tj)
+      for (size_t k = 0; k < c.closure.size(); ++k) {
+        ti[k] = c.closure.tiles()[k].i;
+        tj[k] = c.closure.tiles()[k].j;
+      }
+  });
+}
+int tib_flops(tib_matrix m, int preset, const long* rows, const long* cols, long ne, double* f, double* p1,
+              double* p2) {
+  return guarded([&] {
+    need(m, "matrix");
+    const FactorPlan plan = symbolic_cholesky(m->pattern);
+    const Closure c = symbolic_inversion(select_tiles(plan.filled.layout(), plan.filled, make_request(preset, rows, cols, ne)),
+                                         plan.filled);
+    const Flops fl = count_flops(plan, &c);
+    if (f) *f = fl.factorize;
+    if (p1) *p1 = fl.phase1;
+    if (p2) *p2 = fl.phase2;
+  });
+}
+
+int tib_factorize(tib_matrix m, int device, tib_factor* out) {
+  return guarded([&] {
+    need(m, "matrix");
+    DeviceRt& rt = runtime(device);
+    cudaStream_t s = rt.stream;
+    auto fp = factor_plan_for(m->pattern, device, s);
+    SweepStores st;
+    alloc_factor_stores(st, *fp, 1, device, s);
+    upload_matrix(*m, fp->sym.filled, fp->bp, st.A.p, s);
+    std::vector<BaseTable> tables{make_table(st.A.p, st.L.p, st.P1.p, nullptr, nullptr, st.scratch.p, st.logdet.p, st.status.p)};
+    factor_sweep(*fp, st, s, tables);
+    std::vector<double> parts(static_cast<size_t>(m->layout.N) * fp->nb);
+    CK(cudaMemcpyAsync(parts.data(), st.logdet.p, parts.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    check_status(st.status, 1, m->layout, s);
+    auto* f = new tib_factor_s;
+    f->device = device;
+    f->layout = m->layout;
+    f->plan = fp;
+    f->L = std::move(st.L);
+    f->P1 = std::move(st.P1);
+    f->logdet = reduce_logdet(parts.data(), m->layout.N, fp->nb);
+    *out = f;
+  });
+}
+int tib_factor_info(tib_factor f, long* n, int* b, long* stored) {
+  return guarded([&] {
+    need(f, "factor");
+    if (n) *n = f->layout.n;
+    if (b) *b = f->layout.b;
+    if (stored) *stored = static_cast<long>(f->plan->sym.filled.size());
+  });
+}
+int tib_factor_logdet(tib_factor f, double* out) {
+  return guarded([&] { *out = need(f, "factor")->logdet; });
+}
+int tib_factor_tiles(tib_factor f, int phase, int* ti, int* tj, double* payload) {
+  return guarded([&] {
+    need(f, "factor");
+    if (phase != 1 && phase != 2) throw Error(kErrInvalidArgument, "phase must be 1 (factor) or 2 (phase-1 tiles)");
+    DeviceRt& rt = runtime(f->device);
+    download_tiles(phase == 1 ? f->L : f->P1, f->plan->sym.filled, f->layout.b, f->plan->bp, ti, tj, payload, rt.stream,
+                   phase == 2);
+  });
+}
+int tib_factor_checksum(tib_factor f, uint64_t* out) {
+  return guarded([&] {
+    need(f, "factor");
+    DeviceRt& rt = runtime(f->device);
+    HostBuf h(f->L.n);
+    CK(cudaMemcpyAsync(h.p, f->L.p, h.n * sizeof(double), cudaMemcpyDeviceToHost, rt.stream));
+    CK(cudaStreamSynchronize(rt.stream));
+    *out = checksum_store(h.p, f->plan->sym.filled, f->layout.b, f->plan->bp);
+  });
+}
+int tib_factor_free(tib_factor f) {
+  delete f;
+  return kOk;
+}
+
+int tib_selected_inverse(tib_matrix m, int preset, const long* rows, const long* cols, long ne, int device,
+                         tib_sigma* out) {
+  return guarded([&] {
+    need(m, "matrix");
+    const Request req = make_request(preset, rows, cols, ne);
+    SigmaObj* r = selected_inverse_matrix(*m, req, device);
+    auto* o = new tib_sigma_s;
+    static_cast<SigmaObj&>(*o) = std::move(*r);
+    delete r;
+    *out = o;
+  });
+}
+
+int tib_selected_inverse_of_factor(tib_factor f, int preset, const long* rows, const long* cols, long ne,
+                                   tib_sigma* out) {
+  return guarded([&] {
+    need(f, "factor");
+    DeviceRt& rt = runtime(f->device);
+    cudaStream_t s = rt.stream;
+    const Request req = make_request(preset, rows, cols, ne);
+    const Pattern& F = f->plan->sym.filled;
+    const Closure sel = symbolic_inversion(select_tiles(F.layout(), F, req), F);
+    auto p2 = phase2_plan_for(F, sel, f->device, s);
+    auto* res = new tib_sigma_s;
+    std::unique_ptr<tib_sigma_s> guard(res);
+    res->device = f->device;
+    res->layout = f->layout;
+    res->req = req;
+    res->plan = p2;
+    res->logdet = f->logdet;
+    const size_t tile = static_cast<size_t>(p2->bp) * p2->bp;
+    res->S = DevBuf(p2->sel.closure.size() * tile, f->device, s);
+    res->var = DevBuf(static_cast<size_t>(f->layout.N) * p2->bp, f->device, s);
+    std::vector<BaseTable> tables{make_table(nullptr, f->L.p, f->P1.p, res->S.p, res->var.p, nullptr, nullptr)};
+    phase2_sweep(*p2, s, tables);
+    CK(cudaStreamSynchronize(s));
+    *out = guard.release();
+  });
+}
+
+int tib_sigma_info(tib_sigma sg, long* n, int* b, long* closure_tiles, int* growth) {
+  return guarded([&] {
+    need(sg, "result");
+    if (n) *n = sg->layout.n;
+    if (b) *b = sg->layout.b;
+    if (closure_tiles) *closure_tiles = static_cast<long>(sg->plan->sel.closure.size());
+    if (growth) *growth = sg->plan->sel.growth_warning ? 1 : 0;
+  });
+}
+int tib_sigma_logdet(tib_sigma sg, double* out) {
+  return guarded([&] { *out = need(sg, "result")->logdet; });
+}
+int tib_sigma_diagonal(tib_sigma sg, double* out) {
+  return guarded([&] {
+    need(sg, "result");
+    const Layout& L = sg->layout;
+    for (int i = 0; i < L.N; ++i)
+      if (!sg->plan->sel.closure.has(i, i))
+        throw Error(kErrContract, "entry (" + std::to_string(static_cast<long>(i) * L.b) + ", " +
+                                      std::to_string(static_cast<long>(i) * L.b) + ") lies outside the computed closure");
+    DeviceRt& rt = runtime(sg->device);
+    const int bp = sg->plan->bp;
+    std::vector<double> v(sg->var.n);
+    CK(cudaMemcpyAsync(v.data(), sg->var.p, v.size() * sizeof(double), cudaMemcpyDeviceToHost, rt.stream));
+    CK(cudaStreamSynchronize(rt.stream));
+    for (long r = 0; r < L.n; ++r) out[r] = v[static_cast<size_t>(r / L.b) * bp + static_cast<size_t>(r % L.b)];
+  });
+}
+int tib_sigma_entries(tib_sigma sg, long* count, long* rows, long* cols, double* vals) {
+  return guarded([&] {
+    need(sg, "result");
+    const Layout& L = sg->layout;
+    const Pattern& C = sg->plan->sel.closure;
+    const int bp = sg->plan->bp;
+    const bool want = rows || cols || vals;
+    const double* h = want ? sigma_host(*sg) : nullptr;
+    long k = 0;
+    for_each_request_entry(L, C, sg->plan->sel.requested, sg->req, [&](long r, long c) {
+      const Address a = map_entry_to_tile(L, r, c);
+      const long slot = C.slot(a.tile.i, a.tile.j);
+      if (slot < 0)
+        throw Error(kErrContract, "entry (" + std::to_string(r) + ", " + std::to_string(c) +
+                                      ") lies outside the computed closure");
+      if (want) {
+        if (rows) rows[k] = r;
+        if (cols) cols[k] = c;
+        if (vals)
+          vals[k] = h[static_cast<size_t>(slot) * bp * bp + static_cast<size_t>(a.row_off) * bp + a.col_off];
+      }
+      ++k;
+    });
+    *count = k;
+  });
+}
+int tib_sigma_tiles(tib_sigma sg, int* ti, int* tj, double* payload) {
+  return guarded([&] {
+    need(sg, "result");
+    DeviceRt& rt = runtime(sg->device);
+    download_tiles(sg->S, sg->plan->sel.closure, sg->layout.b, sg->plan->bp, ti, tj, payload, rt.stream, false);
+  });
+}
+int tib_sigma_checksum(tib_sigma sg, uint64_t* out) {
+  return guarded([&] {
+    need(sg, "result");
+    *out = checksum_store(sigma_host(*sg), sg->plan->sel.closure, sg->layout.b, sg->plan->bp);
+  });
+}
+int tib_sigma_free(tib_sigma sg) {
+  delete sg;
+  return kOk;
+}
+
+int tib_selected_inverse_batch(const tib_matrix* ms, int count, int device, double* logdet, double* diag) {
+  return guarded([&] {
+    if (count < 1 || !ms) throw Error(kErrInvalidArgument, "batch needs at least one matrix");
+    const MatrixObj& m0 = *need(ms[0], "matrix");
+    for (int k = 1; k < count; ++k)
+      if (!(need(ms[k], "matrix")->pattern == m0.pattern) || ms[k]->layout.n != m0.layout.n)
+        throw Error(kErrInvalidArgument, "batched matrices must share one tile pattern");
+    DeviceRt& rt = runtime(device);
+    cudaStream_t s = rt.stream;
+    auto fp = factor_plan_for(m0.pattern, device, s);
+    const Pattern& F = fp->sym.filled;
+    Request req;
+    req.preset = kFactorPattern;
+    const Closure sel = symbolic_inversion(select_tiles(F.layout(), F, req), F);
+    auto p2 = phase2_plan_for(F, sel, device, s);
+    const size_t tile = static_cast<size_t>(fp->bp) * fp->bp;
+    SweepStores st;
+    alloc_factor_stores(st, *fp, count, device, s);
+    DevBuf Sg(p2->sel.closure.size() * tile * count, device, s);
+    DevBuf var(static_cast<size_t>(m0.layout.N) * fp->bp * count, device, s);
+    std::vector<BaseTable> tables;
+    const size_t T = F.size();
+    for (int k = 0; k < count; ++k) {
+      upload_matrix(*ms[k], F, fp->bp, st.A.p + T * tile * k, s);
+      tables.push_back(make_table(st.A.p + T * tile * k, st.L.p + T * tile * k, st.P1.p + T * tile * k,
+                                  Sg.p + p2->sel.closure.size() * tile * k, var.p + static_cast<size_t>(m0.layout.N) * fp->bp * k,
+                                  st.scratch.p + tile * k, st.logdet.p + static_cast<size_t>(m0.layout.N) * fp->nb * k,
+                                  st.status.p + k));
+    }
+    factor_sweep(*fp, st, s, tables);
+    phase2_sweep(*p2, s, tables);
+    std::vector<double> parts(static_cast<size_t>(m0.layout.N) * fp->nb * count);
+    std::vector<double> v(var.n);
+    CK(cudaMemcpyAsync(parts.data(), st.logdet.p, parts.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(v.data(), var.p, v.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    check_status(st.status, count, m0.layout, s);
+    const Layout& L = m0.layout;
+    for (int k = 0; k < count; ++k) {
+      if (logdet) logdet[k] = reduce_logdet(parts.data() + static_cast<size_t>(L.N) * fp->nb * k, L.N, fp->nb);
+      if (diag)
+        for (long r = 0; r < L.n; ++r)
+          diag[static_cast<size_t>(k) * L.n + r] =
+              v[static_cast<size_t>(L.N) * fp->bp * k + static_cast<size_t>(r / L.b) * fp->bp + static_cast<size_t>(r % L.b)];
+    }
+  });
+}
+
+int tib_bench_resident(tib_matrix m, int device, int reps, int warmup, double* ms_per_rep, double* ms_factor,
+                       double* ms_phase2, double* logdet) {
+  return guarded([&] {
+    need(m, "matrix");
+    if (reps < 1 || warmup < 0) throw Error(kErrInvalidArgument, "reps >= 1, warmup >= 0");
+    DeviceRt& rt = runtime(device);
+    cudaStream_t s = rt.stream;
+    auto fp = factor_plan_for(m->pattern, device, s);
+    const Pattern& F = fp->sym.filled;
+    Request req;
+    req.preset = kFactorPattern;
+    const Closure sel = symbolic_inversion(select_tiles(F.layout(), F, req), F);
+    auto p2 = phase2_plan_for(F, sel, device, s);
+    const size_t tile = static_cast<size_t>(fp->bp) * fp->bp;
+    SweepStores st;
+    alloc_factor_stores(st, *fp, 1, device, s);
+    DevBuf A0(F.size() * tile, device, s);
+    upload_matrix(*m, F, fp->bp, A0.p, s);
+    DevBuf Sg(p2->sel.closure.size() * tile, device, s);
+    DevBuf var(static_cast<size_t>(m->layout.N) * fp->bp, device, s);
+    std::vector<BaseTable> tables{make_table(st.A.p, st.L.p, st.P1.p, Sg.p, var.p, st.scratch.p, st.logdet.p, st.status.p)};
+    cudaEvent_t e0, e1, e2;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventCreate(&e2));
+    float tf = 0, tp = 0;
+    double total = 0;
+    for (int it = 0; it < warmup + reps; ++it) {
+      CK(cudaMemcpyAsync(st.A.p, A0.p, A0.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      CK(cudaEventRecord(e0, s));
+      factor_sweep(*fp, st, s, tables);
+      CK(cudaEventRecord(e1, s));
+      phase2_sweep(*p2, s, tables);
+      CK(cudaEventRecord(e2, s));
+      CK(cudaEventSynchronize(e2));
+      CK(cudaEventElapsedTime(&tf, e0, e1));
+      CK(cudaEventElapsedTime(&tp, e1, e2));
+      if (it >= warmup) total += tf + tp;
+    }
+    std::vector<double> parts(static_cast<size_t>(m->layout.N) * fp->nb);
+    CK(cudaMemcpyAsync(parts.data(), st.logdet.p, parts.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    check_status(st.status, 1, m->layout, s);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    if (ms_per_rep) *ms_per_rep = total / reps;
+    if (ms_factor) *ms_factor = tf;
+    if (ms_phase2) *ms_phase2 = tp;
+    if (logdet) *logdet = reduce_logdet(parts.data(), m->layout.N, fp->nb);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,332 @@
+// FP64 tensor-core (DMMA) tile-block GEMM for sm_100a.
+//
+// There is no FP64 kind for tcgen05.mma on sm_100a (ptxas rejects it) and no
+// wgmma; the FP64 tensor path on B200 is mma.sync.m8n8k4.f64, which lowers to
+// DMMA.8x8x4 and was measured at 37.2 TFLOP/s chip-wide (profiles/
+// r01_fp64_peak.jsonl) vs 34.2 for DFMA.  So every dense FP64 tile contraction
+// of the path runs through this one block routine:
+//
+//   C[BM x BN] = C0 + sum_s sign_s * op(A_s) op(B_s)       (K = sum of segment ranges)
+//
+// One CTA owns one 64 x 64 output block of a b x b tile and walks every K
+// segment in a fixed order, so the accumulation order is deterministic and no
+// atomics are needed (the reference fixes ascending-k order for bitwise
+// reproducibility, kernels.hpp:26-27; we fix ours the same way).
+//
+// Operands are staged global -> shared with cp.async (16 B, .cg = L2 only)
+// through a STAGES-deep ring; transposed and non-transposed operands land in
+// two padded shared layouts chosen per K chunk, both conflict-free for the
+// 64-bit fragment loads (row stride = 4 mod 16 doubles).  4 warps, each a
+// 32 x 32 sub-block = 4 x 4 m8n8 accumulators (64 registers).
+#pragma once
+
+#include <cstdint>
+
+namespace tib {
+
+constexpr int kBM = 64;
+constexpr int kBN = 64;
+constexpr int kBK = 16;
+constexpr int kStages = 4;
+constexpr int kGemmThreads = 128;
+constexpr int kLdN = kBK + 4;   // [row][k] layout stride (doubles)
+constexpr int kLdT = kBM + 4;   // [k][row] layout stride (doubles)
+constexpr int kStageDoubles = (kBM * kLdN > kBK * kLdT ? kBM * kLdN : kBK * kLdT);
+constexpr int kGemmSmemBytes = kStages * 2 * kStageDoubles * 8;
+
+enum SegFlags : int { kTransA = 1, kTransB = 2, kNegate = 4 };
+
+// Plans are built once per (pattern, request) on the host and must not depend
+// on where the stores live (results get fresh allocations; a batch of
+// matrices shares one plan), so tasks address operands as (store id, offset
+// in doubles); a per-matrix base table resolves them at run time.
+enum StoreId : int {
+  kStoreA = 0,      // working copy of A (receives the Schur updates in place)
+  kStoreL = 1,      // factor tiles L
+  kStoreP1 = 2,     // phase-1 tiles: X_j = L_jj^{-1} on the diagonal, W_kj off it
+  kStoreSigma = 3,  // selected-inverse tiles
+  kStoreVar = 4,    // marginal variances (N * bp)
+  kStoreScratch = 5,
+  kStoreLogdetId = 6,  // logdet partials (see kernels.cuh kStoreLogdet)
+  kStoreStatus = 7,    // DevStatus word of the matrix
+  kStoreNone = 255,
+};
+constexpr int kMaxStores = 8;
+struct BaseTable {
+  double* p[kMaxStores];
+};
+
+// One K segment.  op(A) rows are the task's block rows, op(B) columns the
+// task's block columns; offsets point at the operand matrix origin (a tile or
+// a sub-block of one) with leading dimensions lda/ldb.
+struct Seg {
+  long long a_off, b_off;
+  int lda, ldb;
+  short k_lo, k_hi;  // K range [k_lo, k_hi), multiples of kBK
+  unsigned char flags, a_store, b_store, pad;
+};
+
+enum TaskMode : int {
+  kFull = 0,       // write the whole block to C
+  kSymDiag = 1,    // diagonal block of a symmetric tile: lower part -> C and mirrored
+  kMirror = 2,     // off-diagonal block of a symmetric tile: C and transpose into Cm
+};
+
+struct Task {
+  long long c_off, c0_off, cm_off, diag_off;
+  int ldc, ldc0;
+  int m0, n0;
+  int seg_begin, seg_count;
+  unsigned char mode, c_store, c0_store, cm_store;
+  unsigned char diag_store, pad0, pad1, pad2;
+};
+
+// Resolved forms used by the block routine.
+struct RSeg {
+  const double* A;
+  const double* B;
+  int lda, ldb, k_lo, k_hi, flags, pad;
+};
+struct RTask {
+  double* C;         // block origin in the output
+  const double* C0;  // block origin of the initial value (may alias C), or null
+  double* Cm;        // kMirror: origin of the transposed block
+  double* diag;      // kSymDiag: if non-null receives C[r][r] (marginal variances)
+  int ldc, ldc0;
+  int m0, n0;        // block offsets into op(A) rows / op(B) columns
+  int seg_count, mode;
+};
+
+__device__ __forceinline__ double* resolve(const BaseTable& bt, unsigned char store, long long off) {
+  return store == kStoreNone ? nullptr : bt.p[store] + off;
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// Stage one BK-wide K chunk of segment s (at k0) into shared buffers.
+__device__ __forceinline__ void load_chunk(const RSeg& s, int m0, int n0, int k0, double* As,
+                                           double* Bs, int tid) {
+  // A: BM x BK of op(A); 512 16-byte pieces, 4 per thread.
+  if (!(s.flags & kTransA)) {
+    // op(A)[m][k] = A[m0+m][k]: rows of 16 doubles = 8 pieces.
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int idx = tid + p * kGemmThreads;
+      const int m = idx >> 3, kq = (idx & 7) * 2;
+      cp_async16(As + m * kLdN + kq, s.A + static_cast<size_t>(m0 + m) * s.lda + k0 + kq);
+    }
+  } else {
+    // op(A)[m][k] = A[k][m0+m]: rows of 64 doubles = 32 pieces.
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int idx = tid + p * kGemmThreads;
+      const int k = idx >> 5, mq = (idx & 31) * 2;
+      cp_async16(As + k * kLdT + mq, s.A + static_cast<size_t>(k0 + k) * s.lda + m0 + mq);
+    }
+  }
+  if (!(s.flags & kTransB)) {
+    // op(B)[k][n] = B[k][n0+n]
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int idx = tid + p * kGemmThreads;
+      const int k = idx >> 5, nq = (idx & 31) * 2;
+      cp_async16(Bs + k * kLdT + nq, s.B + static_cast<size_t>(k0 + k) * s.ldb + n0 + nq);
+    }
+  } else {
+    // op(B)[k][n] = B[n0+n][k]
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int idx = tid + p * kGemmThreads;
+      const int n = idx >> 3, kq = (idx & 7) * 2;
+      cp_async16(Bs + n * kLdN + kq, s.B + static_cast<size_t>(n0 + n) * s.ldb + k0 + kq);
+    }
+  }
+}
+
+// Segment sources for gemm_task: plan segments in global memory resolved
+// through a base table, or ready-made segments (e.g. built in shared memory).
+struct GlobalSegs {
+  const Seg* segs;
+  const BaseTable* bt;
+  int count;
+  __device__ __forceinline__ RSeg get(int i) const {
+    const Seg s = segs[i];
+    RSeg r;
+    r.A = bt->p[s.a_store] + s.a_off;
+    r.B = bt->p[s.b_store] + s.b_off;
+    r.lda = s.lda;
+    r.ldb = s.ldb;
+    r.k_lo = s.k_lo;
+    r.k_hi = s.k_hi;
+    r.flags = s.flags;
+    r.pad = 0;
+    return r;
+  }
+};
+struct LocalSegs {
+  const RSeg* segs;
+  int count;
+  __device__ __forceinline__ RSeg get(int i) const { return segs[i]; }
+};
+
+// Runs one task on the calling CTA (kGemmThreads threads).  smem must hold
+// kGemmSmemBytes.  Safe to call repeatedly from a persistent loop: it ends
+// with a __syncthreads so the ring can be reused.
+template <class Src>
+__device__ __forceinline__ void gemm_task(const RTask& t, const Src& src, double* smem) {
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int fr = lane >> 2, fc = lane & 3;
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  // Flattened chunk sequence over segments, walked by a producer cursor.
+  int nchunks = 0;
+  for (int s = 0; s < src.count; ++s) {
+    const RSeg g = src.get(s);
+    nchunks += (g.k_hi - g.k_lo) / kBK;
+  }
+  int ls = 0, lk = 0;
+  RSeg cur;
+  cur.k_hi = 0;
+  cur.k_lo = 0;
+  if (src.count > 0) {
+    cur = src.get(0);
+    lk = cur.k_lo;
+  }
+  auto settle = [&]() {  // move to the next segment with chunks left
+    while (ls < src.count && lk >= cur.k_hi) {
+      ++ls;
+      if (ls < src.count) {
+        cur = src.get(ls);
+        lk = cur.k_lo;
+      }
+    }
+  };
+  settle();
+  uint32_t stage_flags = 0;  // 3 bits per stage
+#pragma unroll
+  for (int st = 0; st < kStages - 1; ++st) {
+    if (st < nchunks) {
+      double* As = smem + st * 2 * kStageDoubles;
+      load_chunk(cur, t.m0, t.n0, lk, As, As + kStageDoubles, tid);
+      stage_flags |= static_cast<uint32_t>(cur.flags & 7) << (3 * st);
+      lk += kBK;
+      settle();
+    }
+    cp_async_commit();
+  }
+
+  for (int it = 0; it < nchunks; ++it) {
+    cp_async_wait<kStages - 2>();
+    __syncthreads();
+    {
+      const int nx = it + kStages - 1;
+      if (nx < nchunks) {
+        const int st = nx % kStages;
+        double* As = smem + st * 2 * kStageDoubles;
+        load_chunk(cur, t.m0, t.n0, lk, As, As + kStageDoubles, tid);
+        stage_flags = (stage_flags & ~(7u << (3 * st))) | (static_cast<uint32_t>(cur.flags & 7) << (3 * st));
+        lk += kBK;
+        settle();
+      }
+      cp_async_commit();
+    }
+    const int st = it % kStages;
+    const int fl = (stage_flags >> (3 * st)) & 7;
+    const double* As = smem + st * 2 * kStageDoubles;
+    const double* Bs = As + kStageDoubles;
+    const double sg = (fl & kNegate) ? -1.0 : 1.0;
+#pragma unroll
+    for (int kk = 0; kk < kBK; kk += 4) {
+      double a[4], b[4];
+      if (fl & kTransA) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = sg * As[(kk + fc) * kLdT + wm + i * 8 + fr];
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = sg * As[(wm + i * 8 + fr) * kLdN + kk + fc];
+      }
+      if (fl & kTransB) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = Bs[(wn + j * 8 + fr) * kLdN + kk + fc];
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = Bs[(kk + fc) * kLdT + wn + j * 8 + fr];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[i], b[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // Epilogue: C = C0 + acc.
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = wm + i * 8 + fr, c = wn + j * 8 + fc * 2;
+      double v0 = acc[i][j][0], v1 = acc[i][j][1];
+      if (t.C0) {
+        const double2 o = __ldcg(reinterpret_cast<const double2*>(t.C0 + static_cast<size_t>(r) * t.ldc0 + c));
+        v0 += o.x;
+        v1 += o.y;
+      }
+      if (t.mode == kFull) {
+        *reinterpret_cast<double2*>(t.C + static_cast<size_t>(r) * t.ldc + c) = make_double2(v0, v1);
+      } else if (t.mode == kMirror) {
+        *reinterpret_cast<double2*>(t.C + static_cast<size_t>(r) * t.ldc + c) = make_double2(v0, v1);
+        t.Cm[static_cast<size_t>(c) * t.ldc + r] = v0;
+        t.Cm[static_cast<size_t>(c + 1) * t.ldc + r] = v1;
+      } else {  // kSymDiag: lower part wins, mirrored exactly
+        if (r >= c) {
+          t.C[static_cast<size_t>(r) * t.ldc + c] = v0;
+          t.C[static_cast<size_t>(c) * t.ldc + r] = v0;
+          if (r == c && t.diag) t.diag[r] = v0;
+        }
+        if (r >= c + 1) {
+          t.C[static_cast<size_t>(r) * t.ldc + c + 1] = v1;
+          t.C[static_cast<size_t>(c + 1) * t.ldc + r] = v1;
+          if (r == c + 1 && t.diag) t.diag[r] = v1;
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ RTask resolve_task(const Task& s, const BaseTable& bt) {
+  RTask t;
+  t.C = resolve(bt, s.c_store, s.c_off);
+  t.C0 = resolve(bt, s.c0_store, s.c0_off);
+  t.Cm = resolve(bt, s.cm_store, s.cm_off);
+  t.diag = resolve(bt, s.diag_store, s.diag_off);
+  t.ldc = s.ldc;
+  t.ldc0 = s.ldc0;
+  t.m0 = s.m0;
+  t.n0 = s.n0;
+  t.seg_count = s.seg_count;
+  t.mode = s.mode;
+  return t;
+}
+
+}  // namespace tib
