@@ -35,6 +35,7 @@
 
 #include "../../include/tileinv_b200.h"
 #include "kernels.cuh"
+#include "plan.hpp"
 #include "planner.hpp"
 
 namespace tib {
@@ -46,7 +47,6 @@ namespace tib {
   } while (0)
 
 static constexpr int kBlk = 64;
-static int padded_b(int b) { return (b + kBlk - 1) / kBlk * kBlk; }
 
 // ---------------------------------------------------------------------------
 // memory
@@ -187,240 +187,73 @@ static DeviceRt& runtime(int device) {
 }
 
 // ---------------------------------------------------------------------------
-// plans
-struct Launch {
-  int begin = 0, count = 0;
-};
-
-static long long tile_off(long slot, int bp) { return static_cast<long long>(slot) * bp * bp; }
-static long long blk_off(long slot, int bp, int p, int q) {
-  return tile_off(slot, bp) + static_cast<long long>(p) * kBlk * bp + static_cast<long long>(q) * kBlk;
-}
-
-static Task make_task(unsigned char c_store, long long c_off, int bp, int m0, int n0, int seg_begin,
-                      int seg_count) {
-  Task t{};
-  t.c_store = c_store;
-  t.c_off = c_off;
-  t.c0_store = kStoreNone;
-  t.cm_store = kStoreNone;
-  t.diag_store = kStoreNone;
-  t.ldc = t.ldc0 = bp;
-  t.m0 = m0;
-  t.n0 = n0;
-  t.seg_begin = seg_begin;
-  t.seg_count = seg_count;
-  t.mode = kFull;
-  return t;
-}
-static Seg make_seg(unsigned char as, long long ao, unsigned char bs, long long bo, int bp, int klo, int khi,
-                    int flags) {
-  Seg s{};
-  s.a_store = as;
-  s.a_off = ao;
-  s.b_store = bs;
-  s.b_off = bo;
-  s.lda = s.ldb = bp;
-  s.k_lo = static_cast<short>(klo);
-  s.k_hi = static_cast<short>(khi);
-  s.flags = static_cast<unsigned char>(flags);
-  return s;
-}
-
-// Graph of one sweep for a given batch size (the base tables it reads live in
-// device memory, so the graph never depends on store addresses).
+// plans: host-built dataflow task lists (plan.cpp), uploaded once per device
+// and replayed through a CUDA graph per batch size.
 struct GraphCache {
   struct Entry {
     cudaGraphExec_t exec = nullptr;
     BaseTable* tables = nullptr;  // device copy of the per-matrix base tables, owned here
+    int* claim = nullptr;         // queue claim counters
   };
   std::map<int, Entry> by_batch;
   Entry& get(int batch) {
     Entry& e = by_batch[batch];
     if (!e.tables) CK(cudaMalloc(reinterpret_cast<void**>(&e.tables), sizeof(BaseTable) * batch));
+    if (!e.claim) CK(cudaMalloc(reinterpret_cast<void**>(&e.claim), 2 * sizeof(int)));
     return e;
   }
   ~GraphCache() {
     for (auto& kv : by_batch) {
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
       if (kv.second.tables) cudaFree(kv.second.tables);
+      if (kv.second.claim) cudaFree(kv.second.claim);
     }
   }
+};
+
+struct DevPlan {
+  DataflowPlan host;
+  int device = -1;
+  int grid = 0;
+  DevArray<DTask> tasks;
+  DevArray<Seg> segs;
+  DevArray<Dep> deps;
+  DevArray<int> sigs;
+  GraphCache graphs;
+  std::mutex mu;
 };
 
 struct FactorPlan2 {
+  FactorPlan sym;  // filled pattern + reference task counts
+  std::shared_ptr<DevPlan> flow;
   Layout L;
-  int bp = 0, nb = 0, cluster = 1;
-  FactorPlan sym;  // filled pattern + counts
-  std::vector<Task> tasks;
-  std::vector<Seg> segs;
-  std::vector<DiagJob> jobs;
-  struct Col {
-    Launch panel, wupd;
-  };
-  std::vector<Col> cols;
-  int device = -1;
-  DevArray<Task> d_tasks;
-  DevArray<Seg> d_segs;
-  DevArray<DiagJob> d_jobs;
-  GraphCache graphs;
-  std::mutex mu;
+  int bp = 0, nb = 0;
 };
 
 struct Phase2Plan {
-  Layout L;
-  int bp = 0, nb = 0;
   Closure sel;
-  std::vector<Task> tasks;
-  std::vector<Seg> segs;
-  struct Col {
-    Launch off, diag;
-  };
-  std::vector<Col> cols;
-  int device = -1;
-  DevArray<Task> d_tasks;
-  DevArray<Seg> d_segs;
-  GraphCache graphs;
-  std::mutex mu;
+  std::shared_ptr<DevPlan> flow;
+  int bp = 0, nb = 0;
 };
 
-static std::shared_ptr<FactorPlan2> build_factor_plan(const Pattern& pattern) {
-  auto plan = std::make_shared<FactorPlan2>();
-  plan->sym = symbolic_cholesky(pattern);
-  const Pattern& F = plan->sym.filled;
-  const Layout& L = F.layout();
-  plan->L = L;
-  const int bp = padded_b(L.b), nb = bp / kBlk;
-  plan->bp = bp;
-  plan->nb = nb;
-  plan->cluster = nb >= 8 ? 16 : nb >= 4 ? 8 : nb >= 2 ? 4 : 1;
-  auto& T = plan->tasks;
-  auto& S = plan->segs;
-  for (int j = 0; j < L.N; ++j) {
-    const long dslot = F.col_start(j);
-    DiagJob job{};
-    job.a_off = job.l_off = job.x_off = tile_off(dslot, bp);
-    job.t_off = 0;
-    job.logdet_off = static_cast<long long>(j) * nb;
-    job.pivot_base = static_cast<long long>(j) * L.b;
-    job.valid_rows = static_cast<int>(std::min<long>(L.b, L.n - static_cast<long>(j) * L.b));
-    job.mode = kFactorInvert;
-    plan->jobs.push_back(job);
-    FactorPlan2::Col col;
-    std::vector<long> ks;  // slots of rows > j
-    std::vector<int> krows;
-    for (const int* r = F.rows_begin(j); r != F.rows_end(j); ++r)
-      if (*r > j) {
-        krows.push_back(*r);
-        ks.push_back(F.slot(*r, j));
-      }
-    // L_kj = A_kj X_j^T (X^T upper: k < n0 + 64)
-    col.panel.begin = static_cast<int>(T.size());
-    for (long sk : ks)
-      for (int p = 0; p < nb; ++p)
-        for (int q = 0; q < nb; ++q) {
-          T.push_back(make_task(kStoreL, blk_off(sk, bp, p, q), bp, p * kBlk, q * kBlk, static_cast<int>(S.size()), 1));
-          S.push_back(make_seg(kStoreA, tile_off(sk, bp), kStoreP1, tile_off(dslot, bp), bp, 0, (q + 1) * kBlk, kTransB));
-        }
-    col.panel.count = static_cast<int>(T.size()) - col.panel.begin;
-    col.wupd.begin = static_cast<int>(T.size());
-    // window update first (it feeds the next diagonal), then W
-    for (size_t ib = 0; ib < krows.size(); ++ib)
-      for (size_t ia = ib; ia < krows.size(); ++ia) {
-        const int a = krows[ia], c = krows[ib];
-        const long ts = F.slot(a, c);
-        if (ts < 0) throw Error(kErrConsistency, "update target outside the filled pattern");
-        for (int p = 0; p < nb; ++p)
-          for (int q = 0; q < (a == c ? p + 1 : nb); ++q) {
-            Task t = make_task(kStoreA, blk_off(ts, bp, p, q), bp, p * kBlk, q * kBlk, static_cast<int>(S.size()), 1);
-            t.c0_store = kStoreA;
-            t.c0_off = t.c_off;
-            T.push_back(t);
-            S.push_back(make_seg(kStoreL, tile_off(ks[ia], bp), kStoreL, tile_off(ks[ib], bp), bp, 0, bp,
-                                 kTransB | kNegate));
-          }
-      }
-    // W_kj = L_kj X_j (X lower: k >= n0)
-    for (long sk : ks)
-      for (int p = 0; p < nb; ++p)
-        for (int q = 0; q < nb; ++q) {
-          T.push_back(make_task(kStoreP1, blk_off(sk, bp, p, q), bp, p * kBlk, q * kBlk, static_cast<int>(S.size()), 1));
-          S.push_back(make_seg(kStoreL, tile_off(sk, bp), kStoreP1, tile_off(dslot, bp), bp, q * kBlk, bp, 0));
-        }
-    col.wupd.count = static_cast<int>(T.size()) - col.wupd.begin;
-    plan->cols.push_back(col);
-  }
-  return plan;
+static int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::atoi(e) : dflt;
 }
+static int crit_workers() { return env_int("TIB_CRIT_WORKERS", 16); }
 
-static std::shared_ptr<Phase2Plan> build_phase2_plan(const Pattern& F, const Closure& sel) {
-  auto plan = std::make_shared<Phase2Plan>();
-  const Layout& L = F.layout();
-  plan->L = L;
-  plan->sel = sel;
-  const Pattern& C = plan->sel.closure;
-  const int bp = padded_b(L.b), nb = bp / kBlk;
-  plan->bp = bp;
-  plan->nb = nb;
-  auto& T = plan->tasks;
-  auto& S = plan->segs;
-  auto cslot = [&](int i, int j) {
-    const long s = C.slot(i, j);
-    if (s < 0)
-      throw Error(kErrConsistency, "operand tile (" + std::to_string(i) + ", " + std::to_string(j) +
-                                       ") missing from the closure");
-    return s;
-  };
-  for (const ColumnWork& cw : plan->sel.columns) {
-    const int i = cw.col;
-    std::vector<int> ks;
-    for (const int* r = F.rows_begin(i); r != F.rows_end(i); ++r)
-      if (*r > i) ks.push_back(*r);
-    Phase2Plan::Col col;
-    col.off.begin = static_cast<int>(T.size());
-    for (int j : cw.offdiag_rows) {
-      const long ts = cslot(j, i);
-      for (int p = 0; p < nb; ++p)
-        for (int q = 0; q < nb; ++q) {
-          T.push_back(make_task(kStoreSigma, blk_off(ts, bp, p, q), bp, p * kBlk, q * kBlk, static_cast<int>(S.size()),
-                                static_cast<int>(ks.size())));
-          for (int k : ks) {
-            const long ms = cslot(std::max(j, k), std::min(j, k));
-            S.push_back(make_seg(kStoreSigma, tile_off(ms, bp), kStoreP1, tile_off(F.slot(k, i), bp), bp, 0, bp,
-                                 (k > j ? kTransA : 0) | kNegate));
-          }
-        }
-    }
-    col.off.count = static_cast<int>(T.size()) - col.off.begin;
-    col.diag.begin = static_cast<int>(T.size());
-    if (cw.diagonal) {
-      const long ds = cslot(i, i);
-      const long xs = F.slot(i, i);
-      for (int p = 0; p < nb; ++p)
-        for (int q = 0; q <= p; ++q) {
-          Task t = make_task(kStoreSigma, blk_off(ds, bp, p, q), bp, p * kBlk, q * kBlk, static_cast<int>(S.size()),
-                             1 + static_cast<int>(ks.size()));
-          if (p == q) {
-            t.mode = kSymDiag;
-            t.diag_store = kStoreVar;
-            t.diag_off = static_cast<long long>(i) * bp + p * kBlk;
-          } else {
-            t.mode = kMirror;
-            t.cm_store = kStoreSigma;
-            t.cm_off = blk_off(ds, bp, q, p);
-          }
-          T.push_back(t);
-          // U U^T = X^T X; rows >= p*64 of X are the only nonzero contributions
-          S.push_back(make_seg(kStoreP1, tile_off(xs, bp), kStoreP1, tile_off(xs, bp), bp, p * kBlk, bp, kTransA));
-          for (int k : ks)
-            S.push_back(make_seg(kStoreP1, tile_off(F.slot(k, i), bp), kStoreSigma, tile_off(cslot(k, i), bp), bp, 0, bp,
-                                 kTransA | kNegate));
-        }
-    }
-    col.diag.count = static_cast<int>(T.size()) - col.diag.begin;
-    plan->cols.push_back(col);
-  }
-  return plan;
+static std::shared_ptr<DevPlan> upload_plan(DataflowPlan&& host, int device, cudaStream_t s) {
+  auto d = std::make_shared<DevPlan>();
+  d->host = std::move(host);
+  d->device = device;
+  d->grid = dataflow_grid(device);
+  if (d->grid <= d->host.q0.workers) throw Error(kErrCuda, "persistent grid too small for the critical queue");
+  d->tasks.upload(d->host.tasks, s);
+  d->segs.upload(d->host.segs, s);
+  d->deps.upload(d->host.deps, s);
+  d->sigs.upload(d->host.sigs, s);
+  CK(cudaStreamSynchronize(s));
+  return d;
 }
 
 // plan caches (keyed by layout + pattern tiles [+ closure tiles])
@@ -444,12 +277,13 @@ static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int 
     auto it = g_fplans.find({device, key});
     if (it != g_fplans.end() && it->second->L.n == pattern.layout().n) return it->second;
   }
-  auto plan = build_factor_plan(pattern);
-  plan->device = device;
-  plan->d_tasks.upload(plan->tasks, s);
-  plan->d_segs.upload(plan->segs, s);
-  plan->d_jobs.upload(plan->jobs, s);
-  CK(cudaStreamSynchronize(s));
+  auto plan = std::make_shared<FactorPlan2>();
+  plan->sym = symbolic_cholesky(pattern);
+  plan->L = plan->sym.filled.layout();
+  plan->flow = upload_plan(build_factor_dataflow(plan->sym.filled, crit_workers(), env_int("TIB_DEFER_W", 2)),
+                           device, s);
+  plan->bp = plan->flow->host.bp;
+  plan->nb = plan->flow->host.nb;
   std::lock_guard<std::mutex> lk(g_plan_mu);
   if (g_fplans.size() > 8) g_fplans.clear();
   g_fplans[{device, key}] = plan;
@@ -464,11 +298,11 @@ static std::shared_ptr<Phase2Plan> phase2_plan_for(const Pattern& F, const Closu
     auto it = g_p2plans.find({device, key});
     if (it != g_p2plans.end()) return it->second;
   }
-  auto plan = build_phase2_plan(F, sel);
-  plan->device = device;
-  plan->d_tasks.upload(plan->tasks, s);
-  plan->d_segs.upload(plan->segs, s);
-  CK(cudaStreamSynchronize(s));
+  auto plan = std::make_shared<Phase2Plan>();
+  plan->sel = sel;
+  plan->flow = upload_plan(build_phase2_dataflow(F, plan->sel, crit_workers()), device, s);
+  plan->bp = plan->flow->host.bp;
+  plan->nb = plan->flow->host.nb;
   std::lock_guard<std::mutex> lk(g_plan_mu);
   if (g_p2plans.size() > 16) g_p2plans.clear();
   g_p2plans[{device, key}] = plan;
@@ -482,39 +316,29 @@ static bool use_graphs() {
   return !(e && e[0] == '0');
 }
 
-static void enqueue_factor_sweep(FactorPlan2& P, const BaseTable* d_tables, int batch, cudaStream_t s) {
-  for (int j = 0; j < P.L.N; ++j) {
-    launch_diag_jobs(P.d_jobs.p + j, 1, d_tables, batch, P.bp, P.cluster, s);
-    const auto& c = P.cols[static_cast<size_t>(j)];
-    launch_gemm_tasks(P.d_tasks.p + c.panel.begin, P.d_segs.p, c.panel.count, d_tables, batch, s);
-    launch_gemm_tasks(P.d_tasks.p + c.wupd.begin, P.d_segs.p, c.wupd.count, d_tables, batch, s);
-  }
-}
-
-static void enqueue_phase2_sweep(Phase2Plan& P, const BaseTable* d_tables, int batch, cudaStream_t s) {
-  for (const auto& c : P.cols) {
-    launch_gemm_tasks(P.d_tasks.p + c.off.begin, P.d_segs.p, c.off.count, d_tables, batch, s);
-    launch_gemm_tasks(P.d_tasks.p + c.diag.begin, P.d_segs.p, c.diag.count, d_tables, batch, s);
-  }
-}
-
-// Uploads the base tables into the plan-owned buffer and runs the sweep,
-// replaying a CUDA graph captured on first use for this batch size.  The
-// graph's only baked-in pointers are plan-owned (tasks, segs, jobs, tables).
-template <class Plan, class Enq>
-static void run_graph(Plan& P, const std::vector<BaseTable>& tables, cudaStream_t s, Enq&& enqueue) {
+// Uploads the base tables into the plan-owned buffer, zeroes each matrix's
+// dependency counters and runs the persistent sweep (captured once per batch
+// size into a CUDA graph; its only baked-in pointers are plan-owned).
+static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(P.mu);
   const int batch = static_cast<int>(tables.size());
   GraphCache::Entry& e = P.graphs.get(batch);
   CK(cudaMemcpyAsync(e.tables, tables.data(), sizeof(BaseTable) * batch, cudaMemcpyHostToDevice, s));
+  for (const BaseTable& t : tables)
+    CK(cudaMemsetAsync(t.p[kStoreCounters], 0, static_cast<size_t>(P.host.counters) * sizeof(int), s));
+  auto enqueue = [&]() {
+    launch_dataflow(P.tasks.p, P.segs.p, P.deps.p, P.sigs.p, P.host.q0, P.host.q1, batch, e.tables, e.claim, P.grid,
+                    s);
+  };
   if (!use_graphs()) {
-    enqueue(e.tables);
+    enqueue();
     CK(cudaGetLastError());
     return;
   }
   if (!e.exec) {
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    enqueue(e.tables);
+    enqueue();
     const cudaError_t le = cudaGetLastError();
     CK(cudaStreamEndCapture(s, &g));
     CK(le);
@@ -587,18 +411,27 @@ static void upload_matrix(const MatrixObj& m, const Pattern& filled, int bp, dou
 }
 
 struct SweepStores {
-  DevBuf A, L, P1, scratch, logdet;
+  DevBuf A, L, P1, scratch, logdet, counters;
   DevBuf status;  // DevStatus per matrix (as doubles storage)
+  long cstride = 0;  // ints of counters per matrix
+  double* ctr(int k) const { return reinterpret_cast<double*>(reinterpret_cast<int*>(counters.p) + cstride * k); }
 };
 
-static void alloc_factor_stores(SweepStores& st, const FactorPlan2& P, int batch, int dev, cudaStream_t s) {
+static DevBuf alloc_counters(long per_matrix, int batch, int dev, cudaStream_t s) {
+  return DevBuf((static_cast<size_t>(per_matrix) * batch + 1) / 2, dev, s);
+}
+
+static void alloc_factor_stores(SweepStores& st, const FactorPlan2& P, int batch, int dev, cudaStream_t s,
+                                long min_counters = 0) {
   const size_t tile = static_cast<size_t>(P.bp) * P.bp;
   const size_t T = P.sym.filled.size();
   st.A = DevBuf(T * tile * batch, dev, s);
   st.L = DevBuf(T * tile * batch, dev, s);
   st.P1 = DevBuf(T * tile * batch, dev, s);
-  st.scratch = DevBuf(tile * batch, dev, s);
-  st.logdet = DevBuf(static_cast<size_t>(P.L.N) * P.nb * batch, dev, s);
+  st.scratch = DevBuf(P.flow->host.scratch_doubles * batch, dev, s);
+  st.logdet = DevBuf(P.flow->host.logdet_doubles * batch, dev, s);
+  st.cstride = std::max<long>(P.flow->host.counters, min_counters);
+  st.counters = alloc_counters(st.cstride, batch, dev, s);
   st.status = DevBuf(static_cast<size_t>(batch), dev, s);
 }
 
@@ -625,21 +458,15 @@ static double reduce_logdet(const double* parts, int N, int nb) {
 // Runs the fused factor sweep for the matrices already resident in their A stores.
 static void factor_sweep(FactorPlan2& P, SweepStores& st, cudaStream_t s, const std::vector<BaseTable>& tables) {
   CK(cudaMemsetAsync(st.status.p, 0xff, tables.size() * sizeof(unsigned long long), s));
-  std::lock_guard<std::mutex> lk(P.mu);
-  run_graph(P, tables, s, [&](const BaseTable* d_tables) {
-    enqueue_factor_sweep(P, d_tables, static_cast<int>(tables.size()), s);
-  });
+  run_flow(*P.flow, tables, s);
 }
 
 static void phase2_sweep(Phase2Plan& P, cudaStream_t s, const std::vector<BaseTable>& tables) {
-  std::lock_guard<std::mutex> lk(P.mu);
-  run_graph(P, tables, s, [&](const BaseTable* d_tables) {
-    enqueue_phase2_sweep(P, d_tables, static_cast<int>(tables.size()), s);
-  });
+  run_flow(*P.flow, tables, s);
 }
 
 static BaseTable make_table(double* A, double* L, double* P1, double* Sg, double* var, double* scratch,
-                            double* logdet, double* status = nullptr) {
+                            double* logdet, double* status, double* counters) {
   BaseTable t{};
   t.p[kStoreA] = A;
   t.p[kStoreL] = L;
@@ -649,6 +476,7 @@ static BaseTable make_table(double* A, double* L, double* P1, double* Sg, double
   t.p[kStoreScratch] = scratch;
   t.p[kStoreLogdet] = logdet;
   t.p[kStoreStatus] = status;
+  t.p[kStoreCounters] = counters;
   return t;
 }
 
@@ -674,7 +502,7 @@ static SigmaObj* selected_inverse_matrix(const MatrixObj& m, const Request& req,
   const Closure sel = symbolic_inversion(select_tiles(F.layout(), F, req), F);
   auto p2 = phase2_plan_for(F, sel, device, s);
   SweepStores st;
-  alloc_factor_stores(st, *fp, 1, device, s);
+  alloc_factor_stores(st, *fp, 1, device, s, p2->flow->host.counters);
   upload_matrix(m, F, fp->bp, st.A.p, s);
   auto* res = new SigmaObj;
   std::unique_ptr<SigmaObj> guard(res);
@@ -685,10 +513,10 @@ static SigmaObj* selected_inverse_matrix(const MatrixObj& m, const Request& req,
   const size_t tile = static_cast<size_t>(fp->bp) * fp->bp;
   res->S = DevBuf(p2->sel.closure.size() * tile, device, s);
   res->var = DevBuf(static_cast<size_t>(m.layout.N) * fp->bp, device, s);
-  std::vector<BaseTable> tables{make_table(st.A.p, st.L.p, st.P1.p, res->S.p, res->var.p, st.scratch.p, st.logdet.p, st.status.p)};
+  std::vector<BaseTable> tables{make_table(st.A.p, st.L.p, st.P1.p, res->S.p, res->var.p, st.scratch.p, st.logdet.p, st.status.p, st.ctr(0))};
   factor_sweep(*fp, st, s, tables);
   phase2_sweep(*p2, s, tables);
-  std::vector<double> parts(static_cast<size_t>(m.layout.N) * fp->nb);
+  std::vector<double> parts(fp->flow->host.logdet_doubles);
   CK(cudaMemcpyAsync(parts.data(), st.logdet.p, parts.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
   check_status(st.status, 1, m.layout, s);
   res->logdet = reduce_logdet(parts.data(), m.layout.N, fp->nb);
@@ -913,7 +741,7 @@ int tib_factorize(tib_matrix m, int device, tib_factor* out) {
     SweepStores st;
     alloc_factor_stores(st, *fp, 1, device, s);
     upload_matrix(*m, fp->sym.filled, fp->bp, st.A.p, s);
-    std::vector<BaseTable> tables{make_table(st.A.p, st.L.p, st.P1.p, nullptr, nullptr, st.scratch.p, st.logdet.p, st.status.p)};
+    std::vector<BaseTable> tables{make_table(st.A.p, st.L.p, st.P1.p, nullptr, nullptr, st.scratch.p, st.logdet.p, st.status.p, st.ctr(0))};
     factor_sweep(*fp, st, s, tables);
     std::vector<double> parts(static_cast<size_t>(m->layout.N) * fp->nb);
     CK(cudaMemcpyAsync(parts.data(), st.logdet.p, parts.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -996,7 +824,8 @@ int tib_selected_inverse_of_factor(tib_factor f, int preset, const long* rows, c
     const size_t tile = static_cast<size_t>(p2->bp) * p2->bp;
     res->S = DevBuf(p2->sel.closure.size() * tile, f->device, s);
     res->var = DevBuf(static_cast<size_t>(f->layout.N) * p2->bp, f->device, s);
-    std::vector<BaseTable> tables{make_table(nullptr, f->L.p, f->P1.p, res->S.p, res->var.p, nullptr, nullptr)};
+    DevBuf ctr = alloc_counters(p2->flow->host.counters, 1, f->device, s);
+    std::vector<BaseTable> tables{make_table(nullptr, f->L.p, f->P1.p, res->S.p, res->var.p, nullptr, nullptr, nullptr, ctr.p)};
     phase2_sweep(*p2, s, tables);
     CK(cudaStreamSynchronize(s));
     *out = guard.release();
@@ -1092,7 +921,7 @@ int tib_selected_inverse_batch(const tib_matrix* ms, int count, int device, doub
     auto p2 = phase2_plan_for(F, sel, device, s);
     const size_t tile = static_cast<size_t>(fp->bp) * fp->bp;
     SweepStores st;
-    alloc_factor_stores(st, *fp, count, device, s);
+    alloc_factor_stores(st, *fp, count, device, s, p2->flow->host.counters);
     DevBuf Sg(p2->sel.closure.size() * tile * count, device, s);
     DevBuf var(static_cast<size_t>(m0.layout.N) * fp->bp * count, device, s);
     std::vector<BaseTable> tables;
@@ -1101,8 +930,8 @@ int tib_selected_inverse_batch(const tib_matrix* ms, int count, int device, doub
       upload_matrix(*ms[k], F, fp->bp, st.A.p + T * tile * k, s);
       tables.push_back(make_table(st.A.p + T * tile * k, st.L.p + T * tile * k, st.P1.p + T * tile * k,
                                   Sg.p + p2->sel.closure.size() * tile * k, var.p + static_cast<size_t>(m0.layout.N) * fp->bp * k,
-                                  st.scratch.p + tile * k, st.logdet.p + static_cast<size_t>(m0.layout.N) * fp->nb * k,
-                                  st.status.p + k));
+                                  st.scratch.p + fp->flow->host.scratch_doubles * k,
+                                  st.logdet.p + fp->flow->host.logdet_doubles * k, st.status.p + k, st.ctr(k)));
     }
     factor_sweep(*fp, st, s, tables);
     phase2_sweep(*p2, s, tables);
@@ -1137,12 +966,12 @@ int tib_bench_resident(tib_matrix m, int device, int reps, int warmup, double* m
     auto p2 = phase2_plan_for(F, sel, device, s);
     const size_t tile = static_cast<size_t>(fp->bp) * fp->bp;
     SweepStores st;
-    alloc_factor_stores(st, *fp, 1, device, s);
+    alloc_factor_stores(st, *fp, 1, device, s, p2->flow->host.counters);
     DevBuf A0(F.size() * tile, device, s);
     upload_matrix(*m, F, fp->bp, A0.p, s);
     DevBuf Sg(p2->sel.closure.size() * tile, device, s);
     DevBuf var(static_cast<size_t>(m->layout.N) * fp->bp, device, s);
-    std::vector<BaseTable> tables{make_table(st.A.p, st.L.p, st.P1.p, Sg.p, var.p, st.scratch.p, st.logdet.p, st.status.p)};
+    std::vector<BaseTable> tables{make_table(st.A.p, st.L.p, st.P1.p, Sg.p, var.p, st.scratch.p, st.logdet.p, st.status.p, st.ctr(0))};
     cudaEvent_t e0, e1, e2;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));

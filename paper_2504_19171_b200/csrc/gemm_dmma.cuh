@@ -22,64 +22,16 @@
 
 #include <cstdint>
 
+#include "taskfmt.hpp"
+
 namespace tib {
 
-constexpr int kBM = 64;
-constexpr int kBN = 64;
-constexpr int kBK = 16;
 constexpr int kStages = 4;
 constexpr int kGemmThreads = 128;
 constexpr int kLdN = kBK + 4;   // [row][k] layout stride (doubles)
 constexpr int kLdT = kBM + 4;   // [k][row] layout stride (doubles)
 constexpr int kStageDoubles = (kBM * kLdN > kBK * kLdT ? kBM * kLdN : kBK * kLdT);
 constexpr int kGemmSmemBytes = kStages * 2 * kStageDoubles * 8;
-
-enum SegFlags : int { kTransA = 1, kTransB = 2, kNegate = 4 };
-
-// Plans are built once per (pattern, request) on the host and must not depend
-// on where the stores live (results get fresh allocations; a batch of
-// matrices shares one plan), so tasks address operands as (store id, offset
-// in doubles); a per-matrix base table resolves them at run time.
-enum StoreId : int {
-  kStoreA = 0,      // working copy of A (receives the Schur updates in place)
-  kStoreL = 1,      // factor tiles L
-  kStoreP1 = 2,     // phase-1 tiles: X_j = L_jj^{-1} on the diagonal, W_kj off it
-  kStoreSigma = 3,  // selected-inverse tiles
-  kStoreVar = 4,    // marginal variances (N * bp)
-  kStoreScratch = 5,
-  kStoreLogdetId = 6,  // logdet partials (see kernels.cuh kStoreLogdet)
-  kStoreStatus = 7,    // DevStatus word of the matrix
-  kStoreNone = 255,
-};
-constexpr int kMaxStores = 8;
-struct BaseTable {
-  double* p[kMaxStores];
-};
-
-// One K segment.  op(A) rows are the task's block rows, op(B) columns the
-// task's block columns; offsets point at the operand matrix origin (a tile or
-// a sub-block of one) with leading dimensions lda/ldb.
-struct Seg {
-  long long a_off, b_off;
-  int lda, ldb;
-  short k_lo, k_hi;  // K range [k_lo, k_hi), multiples of kBK
-  unsigned char flags, a_store, b_store, pad;
-};
-
-enum TaskMode : int {
-  kFull = 0,       // write the whole block to C
-  kSymDiag = 1,    // diagonal block of a symmetric tile: lower part -> C and mirrored
-  kMirror = 2,     // off-diagonal block of a symmetric tile: C and transpose into Cm
-};
-
-struct Task {
-  long long c_off, c0_off, cm_off, diag_off;
-  int ldc, ldc0;
-  int m0, n0;
-  int seg_begin, seg_count;
-  unsigned char mode, c_store, c0_store, cm_store;
-  unsigned char diag_store, pad0, pad1, pad2;
-};
 
 // Resolved forms used by the block routine.
 struct RSeg {
@@ -184,6 +136,13 @@ struct LocalSegs {
 // Runs one task on the calling CTA (kGemmThreads threads).  smem must hold
 // kGemmSmemBytes.  Safe to call repeatedly from a persistent loop: it ends
 // with a __syncthreads so the ring can be reused.
+//
+// Inner loop: the two shared layouts differ only in strides, so fragment
+// addresses are (stage base) + k*sK + row*sM with per-stage strides -- no
+// branches, and the next k-step's fragments are loaded while the current
+// 16 DMMAs issue.  A segment's sign is applied by negating the accumulators
+// when the sign changes between chunks (at most a couple of times per task)
+// instead of per fragment.
 template <class Src>
 __device__ __forceinline__ void gemm_task(const RTask& t, const Src& src, double* smem) {
   const int tid = threadIdx.x;
@@ -207,6 +166,7 @@ __device__ __forceinline__ void gemm_task(const RTask& t, const Src& src, double
   RSeg cur;
   cur.k_hi = 0;
   cur.k_lo = 0;
+  cur.flags = 0;
   if (src.count > 0) {
     cur = src.get(0);
     lk = cur.k_lo;
@@ -234,6 +194,7 @@ __device__ __forceinline__ void gemm_task(const RTask& t, const Src& src, double
     cp_async_commit();
   }
 
+  bool negated = false;
   for (int it = 0; it < nchunks; ++it) {
     cp_async_wait<kStages - 2>();
     __syncthreads();
@@ -251,33 +212,54 @@ __device__ __forceinline__ void gemm_task(const RTask& t, const Src& src, double
     }
     const int st = it % kStages;
     const int fl = (stage_flags >> (3 * st)) & 7;
-    const double* As = smem + st * 2 * kStageDoubles;
-    const double* Bs = As + kStageDoubles;
-    const double sg = (fl & kNegate) ? -1.0 : 1.0;
+    const bool neg = fl & kNegate;
+    if (neg != negated) {
 #pragma unroll
-    for (int kk = 0; kk < kBK; kk += 4) {
-      double a[4], b[4];
-      if (fl & kTransA) {
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = sg * As[(kk + fc) * kLdT + wm + i * 8 + fr];
-      } else {
+        for (int j = 0; j < 4; ++j) {
+          acc[i][j][0] = -acc[i][j][0];
+          acc[i][j][1] = -acc[i][j][1];
+        }
+      negated = neg;
+    }
+    // element (row, k) of the A chunk is at As[k * aK + row * aM]; (k, col) of B at Bs[k * bK + col * bN]
+    const int aK = (fl & kTransA) ? kLdT : 1, aM = (fl & kTransA) ? 1 : kLdN;
+    const int bK = (fl & kTransB) ? 1 : kLdT, bN = (fl & kTransB) ? kLdN : 1;
+    const double* Ap = smem + st * 2 * kStageDoubles + fc * aK + (wm + fr) * aM;
+    const double* Bp = smem + st * 2 * kStageDoubles + kStageDoubles + fc * bK + (wn + fr) * bN;
+    double a[2][4], b[2][4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = sg * As[(wm + i * 8 + fr) * kLdN + kk + fc];
-      }
-      if (fl & kTransB) {
+    for (int i = 0; i < 4; ++i) {
+      a[0][i] = Ap[i * 8 * aM];
+      b[0][i] = Bp[i * 8 * bN];
+    }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) b[j] = Bs[(wn + j * 8 + fr) * kLdN + kk + fc];
-      } else {
+    for (int ks = 0; ks < kBK / 4; ++ks) {
+      const int cb = ks & 1;
+      if (ks + 1 < kBK / 4) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) b[j] = Bs[(kk + fc) * kLdT + wn + j * 8 + fr];
+        for (int i = 0; i < 4; ++i) {
+          a[cb ^ 1][i] = Ap[(ks + 1) * 4 * aK + i * 8 * aM];
+          b[cb ^ 1][i] = Bp[(ks + 1) * 4 * bK + i * 8 * bN];
+        }
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[i], b[j]);
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[cb][i], b[cb][j]);
     }
   }
   cp_async_wait<0>();
+  if (negated) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        acc[i][j][0] = -acc[i][j][0];
+        acc[i][j][1] = -acc[i][j][1];
+      }
+  }
 
   // Epilogue: C = C0 + acc.
 #pragma unroll

@@ -1,0 +1,48 @@
+// Dataflow task plans for the two device sweeps (kernels.cu dataflow_kernel).
+//
+// A plan is a pointer-free task list (store id + offset addressing, see
+// taskfmt.hpp) with per-task dependency lists and completion signals on
+// integer counters.  It is built once per tile pattern (and per closure for
+// phase 2), cached, and shared by every matrix with that pattern -- including
+// all members of a batch.  Building it is pure integer work on the host.
+#pragma once
+
+#include <vector>
+
+#include "planner.hpp"
+#include "taskfmt.hpp"
+
+namespace tib {
+
+struct DataflowPlan {
+  Layout L;
+  int bp = 0, nb = 0;
+  std::vector<DTask> tasks;  // queue 0 (critical chain) then queue 1 (bulk)
+  std::vector<Seg> segs;
+  std::vector<Dep> deps;
+  std::vector<int> sigs;
+  QueueDesc q0{}, q1{};
+  long counters = 0;          // ints per matrix
+  size_t scratch_doubles = 0; // per matrix
+  size_t logdet_doubles = 0;  // per matrix
+  double task_flops = 0;      // FLOPs actually executed by the block tasks (2 per FMA)
+};
+
+// Fused factorization + phase 1 over the FILLED pattern: per column, the
+// diagonal-tile chain (64x64 leaves + intra-tile panel / trailing / inverse
+// rows) on queue 0; panel GEMMs L_kj = A_kj X_j^T, Schur updates (critical
+// column first) and deferred W_kj = L_kj X_j on queue 1.
+DataflowPlan build_factor_dataflow(const Pattern& filled, int crit_workers, int defer_w);
+
+// Phase 2 over a closure: per column descending, off-diagonal targets split
+// into an early part and the k == j term, diagonal targets into LAUUM + early
+// terms and the first-row term; the first-row chain is queue 0.
+DataflowPlan build_phase2_dataflow(const Pattern& filled, const Closure& sel, int crit_workers);
+
+// Simulates the plan in its global emission order (queue 0 and queue 1 are
+// both subsequences of it) and throws ConsistencyError if any dependency is
+// not produced by an earlier task -- the property that makes in-order claiming
+// deadlock-free.
+void validate_dataflow(const DataflowPlan& plan, const std::vector<int>& global_order);
+
+}  // namespace tib
