@@ -26,6 +26,7 @@
 #include <atomic>
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -46,7 +47,6 @@ namespace tib {
     if (e_ != cudaSuccess) throw Error(kErrCuda, std::string(#x) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
-static constexpr int kBlk = 64;
 
 // ---------------------------------------------------------------------------
 // memory
@@ -280,7 +280,8 @@ static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int 
   auto plan = std::make_shared<FactorPlan2>();
   plan->sym = symbolic_cholesky(pattern);
   plan->L = plan->sym.filled.layout();
-  plan->flow = upload_plan(build_factor_dataflow(plan->sym.filled, crit_workers(), env_int("TIB_DEFER_W", 2)),
+  plan->flow = upload_plan(build_factor_dataflow(plan->sym.filled, crit_workers(), env_int("TIB_DEFER_W", 2),
+                                                  env_int("TIB_FAT_LEAF", 0) != 0),
                            device, s);
   plan->bp = plan->flow->host.bp;
   plan->nb = plan->flow->host.nb;
@@ -316,6 +317,37 @@ static bool use_graphs() {
   return !(e && e[0] == '0');
 }
 
+// Task trace (TIB_TRACE=<prefix>): per executed task claim / ready / done
+// globaltimer stamps + (task, matrix, SM), written to <prefix>.<n>.bin
+// together with the plan's task kinds; tools/trace_report.py reads them.
+static const char* trace_prefix() {
+  const char* e = std::getenv("TIB_TRACE");
+  return e && *e ? e : nullptr;
+}
+static std::atomic<int> g_trace_seq{0};
+
+static void write_trace(DevPlan& P, int batch, unsigned long long* d_trace, cudaStream_t s) {
+  const size_t n = static_cast<size_t>(P.host.tasks.size()) * batch * 4;
+  std::vector<unsigned long long> h(n);
+  CK(cudaMemcpyAsync(h.data(), d_trace, n * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const std::string path = std::string(trace_prefix()) + "." + std::to_string(g_trace_seq++) + ".bin";
+  FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) return;
+  const long long hdr[4] = {static_cast<long long>(P.host.tasks.size()), batch, P.host.q0.count, P.host.nb};
+  std::fwrite(hdr, sizeof(hdr), 1, f);
+  std::vector<unsigned char> kinds(P.host.tasks.size());
+  std::vector<int> segc(P.host.tasks.size());
+  for (size_t i = 0; i < kinds.size(); ++i) {
+    kinds[i] = P.host.tasks[i].kind;
+    segc[i] = P.host.tasks[i].seg_count;
+  }
+  std::fwrite(kinds.data(), 1, kinds.size(), f);
+  std::fwrite(segc.data(), sizeof(int), segc.size(), f);
+  std::fwrite(h.data(), 8, n, f);
+  std::fclose(f);
+}
+
 // Uploads the base tables into the plan-owned buffer, zeroes each matrix's
 // dependency counters and runs the persistent sweep (captured once per batch
 // size into a CUDA graph; its only baked-in pointers are plan-owned).
@@ -326,6 +358,18 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
   CK(cudaMemcpyAsync(e.tables, tables.data(), sizeof(BaseTable) * batch, cudaMemcpyHostToDevice, s));
   for (const BaseTable& t : tables)
     CK(cudaMemsetAsync(t.p[kStoreCounters], 0, static_cast<size_t>(P.host.counters) * sizeof(int), s));
+  if (trace_prefix()) {
+    unsigned long long* d_trace = nullptr;
+    const size_t n = static_cast<size_t>(P.host.tasks.size()) * batch * 4;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&d_trace), n * 8, s));
+    CK(cudaMemsetAsync(d_trace, 0, n * 8, s));
+    launch_dataflow(P.tasks.p, P.segs.p, P.deps.p, P.sigs.p, P.host.q0, P.host.q1, batch, e.tables, e.claim, P.grid,
+                    s, d_trace);
+    CK(cudaGetLastError());
+    write_trace(P, batch, d_trace, s);
+    CK(cudaFreeAsync(d_trace, s));
+    return;
+  }
   auto enqueue = [&]() {
     launch_dataflow(P.tasks.p, P.segs.p, P.deps.p, P.sigs.p, P.host.q0, P.host.q1, batch, e.tables, e.claim, P.grid,
                     s);

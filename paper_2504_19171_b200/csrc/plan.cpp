@@ -97,7 +97,7 @@ void validate_dataflow(const DataflowPlan& plan, const std::vector<int>& order) 
   }
 }
 
-DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer_w) {
+DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer_w, bool fat_leaf) {
   DataflowPlan P;
   P.L = F.layout();
   const Layout& L = P.L;
@@ -150,10 +150,24 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
     const int U = ord[static_cast<size_t>(ds)];
     const int valid = static_cast<int>(std::min<long>(L.b, L.n - static_cast<long>(j) * L.b));
     // ---- diagonal-tile chain (queue 0): blocked POTRF + TRTRI of tile (j, j)
+    // Fat leaf: factor + invert block (kk, kk), then (kk + 1 < nb) the next
+    // panel block L(kk+1, kk) = A(kk+1, kk) X_kk^T and the next diagonal block
+    // update A(kk+1, kk+1) -= L(kk+1, kk) L(kk+1, kk)^T in the same task, so the
+    // tile's diagonal chain advances one block per task.
     auto leaf = [&](int kk) {
-      DTask& t = B.add(0, {{aord(ds, kk, kk), U + kk}}, {lblk(ds, kk, kk), lfin(ds), xblk(j, kk, kk), xfin(j)});
+      std::vector<Dep> d{{aord(ds, kk, kk), U + kk}};
+      std::vector<int> sg{lblk(ds, kk, kk), lfin(ds), xblk(j, kk, kk), xfin(j)};
+      const bool fat = fat_leaf && kk + 1 < nb;
+      if (fat) {
+        d.push_back({aord(ds, kk + 1, kk), U + kk});
+        d.push_back({aord(ds, kk + 1, kk + 1), U + kk});
+        sg.push_back(lblk(ds, kk + 1, kk));
+        sg.push_back(lfin(ds));
+        sg.push_back(aord(ds, kk + 1, kk + 1));
+      }
+      DTask& t = B.add(0, d, sg);
       t.kind = kLeafTask;
-      t.mode = 0;
+      t.mode = fat ? 2 : 0;
       t.c_off = t.c0_off = t.cm_off = blk_off(ds, bp, kk, kk);
       t.diag_off = static_cast<long long>(j) * nb + kk;
       t.m0 = valid - kk * kB;
@@ -161,6 +175,7 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
       t.seg_count = nb - 1 - kk;  // blocks to zero right of the diagonal block
       t.ldc = t.ldc0 = bp;
       P.task_flops += 2.0 * (kB * kB * kB / 6.0) * 2;  // chol + inverse of the leaf
+      if (fat) P.task_flops += 2.0 * kB * kB * kB * 2;
     };
     auto paneld = [&](int i, int kk) {
       DTask& t = B.add(0, {{lblk(ds, kk, kk), 1}, {aord(ds, i, kk), U + kk}}, {lblk(ds, i, kk), lfin(ds)});
@@ -198,7 +213,7 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
     };
     for (int kk = 0; kk < nb; ++kk) {
       leaf(kk);
-      if (kk + 1 < nb) {
+      if (!fat_leaf && kk + 1 < nb) {
         paneld(kk + 1, kk);
         traild(kk + 1, kk + 1, kk);
       }

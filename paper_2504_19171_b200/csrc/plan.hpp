@@ -32,7 +32,8 @@ struct DataflowPlan {
 // diagonal-tile chain (64x64 leaves + intra-tile panel / trailing / inverse
 // rows) on queue 0; panel GEMMs L_kj = A_kj X_j^T, Schur updates (critical
 // column first) and deferred W_kj = L_kj X_j on queue 1.
-DataflowPlan build_factor_dataflow(const Pattern& filled, int crit_workers, int defer_w);
+// fat_leaf fuses the next panel block and diagonal-block update into the leaf task.
+DataflowPlan build_factor_dataflow(const Pattern& filled, int crit_workers, int defer_w, bool fat_leaf);
 
 // Phase 2 over a closure: per column descending, off-diagonal targets split
 // into an early part and the k == j term, diagonal targets into LAUUM + early
