@@ -127,7 +127,26 @@ int tib_sigma_free(tib_sigma s);
 int tib_selected_inverse_batch(const tib_matrix* ms, int count, int device, double* logdet,
                                double* diag);
 
+/* ---- dataflow plans (host only; inspection and CPU-side simulation) -------- */
+/* Builds the device task plan of one sweep (which = 0: fused factorization +
+ * phase 1, which = 1: phase 2 for the request) WITHOUT a GPU and copies it
+ * out.  sizes[0..9] = {tasks, queue-0 tasks, segments, deps, signals,
+ * counters, bp, scratch doubles, executed FLOPs, sizeof(DTask)}; call with
+ * NULL buffers to query.  Layouts are the POD structs of taskfmt.hpp.        */
+typedef struct tib_resident_s* tib_resident;
+int tib_plan_export(tib_matrix m, int preset, const long* rows, const long* cols, long nentries, int which,
+                    int crit_workers, double* sizes, void* tasks, void* segs, void* deps, void* sigs);
+
 /* ---- timing support (bench.py) -------------------------------------------- */
+/* A device-resident copy of m with all sweep stores allocated; each run
+ * re-copies A on device and executes the fused factorization + selected
+ * inversion (pattern) `reps` times.  Times are CUDA events on the library
+ * stream: total over reps and the two sweeps of the last rep.                */
+int tib_resident_create(tib_matrix m, int device, tib_resident* out);
+int tib_resident_run(tib_resident r, int reps, double* ms_total, double* ms_factor, double* ms_phase2);
+int tib_resident_info(tib_resident r, double* task_model_flops, double* executed_flops, double* logdet,
+                      long* kernel_launches_per_rep);
+int tib_resident_free(tib_resident r);
 /* Device-resident run: uploads m once, then `reps` times runs the fused
  * factorize + selected inversion (pattern) from the resident copy; returns
  * the per-rep device time in ms (CUDA events on the sweep stream) and the

@@ -10,6 +10,10 @@
 //   ref_driver bench  n w t b seed workers [density]
 //       -> one JSON line {factorize_s, phase1_s, phase2_s, total_s, gflop, ...}
 //   ref_driver dump   n w t b seed workers out_prefix [density]
+//   ref_driver symbolic n w t b seed density selection
+//       -> {"factor": [[i,j],...], "closure": [[i,j],...], "requested": [...],
+//           "columns": [[col, diag, [rows...]], ...], "growth_warning": b}
+//          selection = diagonal | pattern | all | r,c;r,c;...
 //       -> <prefix>.diag.f64 (n doubles), <prefix>.sigma.f64 (closure tiles,
 //          column-major tile order, each b*b row-major) and a JSON line.
 #include <chrono>
@@ -64,7 +68,59 @@ static Flops count_flops(const FactorPlan& plan, const SelectedTileSet& sel,
   return f;
 }
 
+static void print_tiles(const char* name, const std::vector<TileCoord>& t) {
+  std::printf("\"%s\": [", name);
+  for (size_t k = 0; k < t.size(); ++k) std::printf("%s[%d,%d]", k ? "," : "", t[k].i, t[k].j);
+  std::printf("]");
+}
+
+static int symbolic_main(int argc, char** argv) {
+  const long n = std::atol(argv[2]), w = std::atol(argv[3]), t = std::atol(argv[4]);
+  const int b = std::atoi(argv[5]);
+  const unsigned long long seed = std::strtoull(argv[6], nullptr, 10);
+  const double density = std::atof(argv[7]);
+  const std::string sel = argc > 8 ? argv[8] : "pattern";
+  SelectionRequest req;
+  if (sel == "diagonal") req = SelectionRequest::diagonal();
+  else if (sel == "pattern") req = SelectionRequest::factor_pattern();
+  else if (sel == "all") req = SelectionRequest::all();
+  else {
+    std::vector<std::pair<long, long>> e;
+    size_t pos = 0;
+    while (pos < sel.size()) {
+      size_t semi = sel.find(';', pos);
+      if (semi == std::string::npos) semi = sel.size();
+      const std::string item = sel.substr(pos, semi - pos);
+      const size_t comma = item.find(',');
+      e.emplace_back(std::atol(item.substr(0, comma).c_str()), std::atol(item.substr(comma + 1).c_str()));
+      pos = semi + 1;
+    }
+    req = SelectionRequest::of(e);
+  }
+  GeneratedMatrix gen = generate_arrowhead({n, w, t, density, seed}, b);
+  const FactorPlan plan = symbolic_cholesky(gen.matrix.pattern);
+  const std::vector<TileCoord> tiles = select_tiles(gen.matrix.layout, plan.filled, req);
+  const SelectedTileSet s = symbolic_inversion(tiles, plan.filled);
+  std::printf("{");
+  print_tiles("factor", plan.filled.tiles());
+  std::printf(", ");
+  print_tiles("closure", s.closure.tiles());
+  std::printf(", ");
+  print_tiles("requested", s.requested);
+  std::printf(", \"columns\": [");
+  for (size_t k = 0; k < s.columns.size(); ++k) {
+    std::printf("%s[%d,%d,[", k ? "," : "", s.columns[k].col, s.columns[k].diagonal ? 1 : 0);
+    for (size_t r = 0; r < s.columns[k].offdiag_rows.size(); ++r)
+      std::printf("%s%d", r ? "," : "", s.columns[k].offdiag_rows[r]);
+    std::printf("]]");
+  }
+  std::printf("], \"growth_warning\": %s, \"tasks\": %zu}\n", s.growth_warning ? "true" : "false",
+              plan.tasks.size());
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc >= 8 && std::string(argv[1]) == "symbolic") return symbolic_main(argc, argv);
   if (argc < 8) {
     std::fprintf(stderr, "usage: ref_driver bench|dump n w t b seed workers [prefix] [density]\n");
     return 2;

@@ -437,3 +437,75 @@ __all__ = [
     "selected_inverse_of_factor", "write_matrix_market", "selected_inverse_batch", "factor_pattern",
     "closure_tiles", "task_flops", "bench_resident", "device_count",
 ]
+
+
+# ---- dataflow plan inspection (host only) and resident timing sessions --------
+
+DTASK_DTYPE = np.dtype({
+    "names": ["c_off", "c0_off", "cm_off", "diag_off", "ldc", "ldc0", "m0", "n0", "seg_begin", "seg_count",
+              "dep_begin", "sig_begin", "dep_count", "sig_count", "kind", "mode", "c_store", "c0_store",
+              "cm_store", "diag_store"],
+    "formats": ["<i8"] * 4 + ["<i4"] * 8 + ["<u2"] * 2 + ["u1"] * 6,
+    "offsets": [0, 8, 16, 24, 32, 36, 40, 44, 48, 52, 56, 60, 64, 66, 68, 69, 70, 71, 72, 73],
+    "itemsize": 80,
+})
+SEG_DTYPE = np.dtype({
+    "names": ["a_off", "b_off", "lda", "ldb", "k_lo", "k_hi", "flags", "a_store", "b_store"],
+    "formats": ["<i8", "<i8", "<i4", "<i4", "<i2", "<i2", "u1", "u1", "u1"],
+    "offsets": [0, 8, 16, 20, 24, 26, 28, 29, 30],
+    "itemsize": 32,
+})
+DEP_DTYPE = np.dtype([("counter", "<i4"), ("value", "<i4")])
+
+
+def plan_export(matrix: Matrix, selection="pattern", which: int = 0, crit_workers: int = 16) -> dict:
+    """Host-built dataflow plan of one device sweep (0: factorization + phase 1,
+    1: phase 2 for `selection`) as numpy arrays; no GPU needed."""
+    preset, rows, cols, ne = _request(selection)
+    sizes = np.zeros(10, np.float64)
+    dptr = sizes.ctypes.data_as(C.POINTER(C.c_double))
+    _check(lib.tib_plan_export(matrix._h, preset, _lp(rows), _lp(cols), ne, which, crit_workers, dptr,
+                               None, None, None, None))
+    nt, nq0, ns, nd, nsig, ncnt, bp, scratch, flops, tsz = sizes.tolist()
+    if int(tsz) != DTASK_DTYPE.itemsize:
+        raise TileinvError(f"DTask layout mismatch: {int(tsz)} vs {DTASK_DTYPE.itemsize}")
+    tasks = np.zeros(int(nt), DTASK_DTYPE)
+    segs = np.zeros(int(ns), SEG_DTYPE)
+    deps = np.zeros(int(nd), DEP_DTYPE)
+    sigs = np.zeros(int(nsig), np.int32)
+    _check(lib.tib_plan_export(matrix._h, preset, _lp(rows), _lp(cols), ne, which, crit_workers, dptr,
+                               tasks.ctypes.data_as(C.c_void_p), segs.ctypes.data_as(C.c_void_p),
+                               deps.ctypes.data_as(C.c_void_p), sigs.ctypes.data_as(C.c_void_p)))
+    return {"tasks": tasks, "segs": segs, "deps": deps, "sigs": sigs, "q0": int(nq0), "counters": int(ncnt),
+            "bp": int(bp), "scratch_doubles": int(scratch), "executed_flops": flops}
+
+
+class Resident:
+    """Device-resident copy of a matrix with every sweep store allocated; run()
+    times `reps` fused factorize + selected-inversion sweeps with CUDA events on
+    the library stream (the bench's device-side measurement)."""
+
+    def __init__(self, matrix: Matrix, device: int = 0):
+        h = _new_handle()
+        _check(lib.tib_resident_create(matrix._h, device, C.byref(h)))
+        self._h = h
+
+    def run(self, reps: int = 1):
+        tot, f, p = C.c_double(), C.c_double(), C.c_double()
+        _check(lib.tib_resident_run(self._h, reps, C.byref(tot), C.byref(f), C.byref(p)))
+        return tot.value, f.value, p.value
+
+    def info(self):
+        m, e, ld, n = C.c_double(), C.c_double(), C.c_double(), C.c_long()
+        _check(lib.tib_resident_info(self._h, C.byref(m), C.byref(e), C.byref(ld), C.byref(n)))
+        return {"task_model_flops": m.value, "executed_flops": e.value, "logdet": ld.value,
+                "kernel_launches_per_rep": n.value}
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib.tib_resident_free(h)
+            self._h = None
+
+
+__all__ += ["plan_export", "Resident", "DTASK_DTYPE", "SEG_DTYPE", "DEP_DTYPE"]

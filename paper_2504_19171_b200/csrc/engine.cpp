@@ -995,56 +995,149 @@ int tib_selected_inverse_batch(const tib_matrix* ms, int count, int device, doub
   });
 }
 
-int tib_bench_resident(tib_matrix m, int device, int reps, int warmup, double* ms_per_rep, double* ms_factor,
-                       double* ms_phase2, double* logdet) {
+int tib_plan_export(tib_matrix m, int preset, const long* rows, const long* cols, long ne, int which,
+                    int crit_workers, double* sizes, void* tasks, void* segs, void* deps, void* sigs) {
   return guarded([&] {
     need(m, "matrix");
-    if (reps < 1 || warmup < 0) throw Error(kErrInvalidArgument, "reps >= 1, warmup >= 0");
+    if (which != 0 && which != 1) throw Error(kErrInvalidArgument, "which must be 0 (factor) or 1 (phase 2)");
+    if (crit_workers < 1) throw Error(kErrInvalidArgument, "at least one reserved critical-queue worker");
+    const FactorPlan sym = symbolic_cholesky(m->pattern);
+    DataflowPlan P;
+    if (which == 0) {
+      P = build_factor_dataflow(sym.filled, crit_workers, env_int("TIB_DEFER_W", 2), env_int("TIB_FAT_LEAF", 0) != 0);
+    } else {
+      const Closure sel =
+          symbolic_inversion(select_tiles(sym.filled.layout(), sym.filled, make_request(preset, rows, cols, ne)), sym.filled);
+      P = build_phase2_dataflow(sym.filled, sel, crit_workers);
+    }
+    if (sizes) {
+      sizes[0] = static_cast<double>(P.tasks.size());
+      sizes[1] = P.q0.count;
+      sizes[2] = static_cast<double>(P.segs.size());
+      sizes[3] = static_cast<double>(P.deps.size());
+      sizes[4] = static_cast<double>(P.sigs.size());
+      sizes[5] = static_cast<double>(P.counters);
+      sizes[6] = P.bp;
+      sizes[7] = static_cast<double>(P.scratch_doubles);
+      sizes[8] = P.task_flops;
+      sizes[9] = sizeof(DTask);
+    }
+    if (tasks) std::memcpy(tasks, P.tasks.data(), P.tasks.size() * sizeof(DTask));
+    if (segs) std::memcpy(segs, P.segs.data(), P.segs.size() * sizeof(Seg));
+    if (deps) std::memcpy(deps, P.deps.data(), P.deps.size() * sizeof(Dep));
+    if (sigs) std::memcpy(sigs, P.sigs.data(), P.sigs.size() * sizeof(int));
+  });
+}
+
+}  // extern "C"
+
+struct tib_resident_s {
+  int device = 0;
+  Layout layout;
+  std::shared_ptr<FactorPlan2> fp;
+  std::shared_ptr<Phase2Plan> p2;
+  SweepStores st;
+  DevBuf A0, Sg, var;
+  std::vector<BaseTable> tables;
+  double logdet = 0;
+  double model_flops = 0;
+};
+
+extern "C" {
+
+int tib_resident_create(tib_matrix m, int device, tib_resident* out) {
+  return guarded([&] {
+    need(m, "matrix");
     DeviceRt& rt = runtime(device);
     cudaStream_t s = rt.stream;
-    auto fp = factor_plan_for(m->pattern, device, s);
-    const Pattern& F = fp->sym.filled;
+    auto r = std::make_unique<tib_resident_s>();
+    r->device = device;
+    r->layout = m->layout;
+    r->fp = factor_plan_for(m->pattern, device, s);
+    const Pattern& F = r->fp->sym.filled;
     Request req;
     req.preset = kFactorPattern;
     const Closure sel = symbolic_inversion(select_tiles(F.layout(), F, req), F);
-    auto p2 = phase2_plan_for(F, sel, device, s);
-    const size_t tile = static_cast<size_t>(fp->bp) * fp->bp;
-    SweepStores st;
-    alloc_factor_stores(st, *fp, 1, device, s, p2->flow->host.counters);
-    DevBuf A0(F.size() * tile, device, s);
-    upload_matrix(*m, F, fp->bp, A0.p, s);
-    DevBuf Sg(p2->sel.closure.size() * tile, device, s);
-    DevBuf var(static_cast<size_t>(m->layout.N) * fp->bp, device, s);
-    std::vector<BaseTable> tables{make_table(st.A.p, st.L.p, st.P1.p, Sg.p, var.p, st.scratch.p, st.logdet.p, st.status.p, st.ctr(0))};
-    cudaEvent_t e0, e1, e2;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
-    CK(cudaEventCreate(&e2));
-    float tf = 0, tp = 0;
-    double total = 0;
-    for (int it = 0; it < warmup + reps; ++it) {
-      CK(cudaMemcpyAsync(st.A.p, A0.p, A0.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-      CK(cudaEventRecord(e0, s));
-      factor_sweep(*fp, st, s, tables);
-      CK(cudaEventRecord(e1, s));
-      phase2_sweep(*p2, s, tables);
-      CK(cudaEventRecord(e2, s));
-      CK(cudaEventSynchronize(e2));
-      CK(cudaEventElapsedTime(&tf, e0, e1));
-      CK(cudaEventElapsedTime(&tp, e1, e2));
-      if (it >= warmup) total += tf + tp;
+    r->p2 = phase2_plan_for(F, sel, device, s);
+    const Flops fl = count_flops(r->fp->sym, &r->p2->sel);
+    r->model_flops = fl.total();
+    const size_t tile = static_cast<size_t>(r->fp->bp) * r->fp->bp;
+    alloc_factor_stores(r->st, *r->fp, 1, device, s, r->p2->flow->host.counters);
+    r->A0 = DevBuf(F.size() * tile, device, s);
+    upload_matrix(*m, F, r->fp->bp, r->A0.p, s);
+    r->Sg = DevBuf(r->p2->sel.closure.size() * tile, device, s);
+    r->var = DevBuf(static_cast<size_t>(m->layout.N) * r->fp->bp, device, s);
+    r->tables = {make_table(r->st.A.p, r->st.L.p, r->st.P1.p, r->Sg.p, r->var.p, r->st.scratch.p, r->st.logdet.p,
+                            r->st.status.p, r->st.ctr(0))};
+    CK(cudaStreamSynchronize(s));
+    *out = r.release();
+  });
+}
+
+int tib_resident_run(tib_resident r, int reps, double* ms_total, double* ms_factor, double* ms_phase2) {
+  return guarded([&] {
+    need(r, "resident");
+    if (reps < 1) throw Error(kErrInvalidArgument, "reps >= 1");
+    DeviceRt& rt = runtime(r->device);
+    cudaStream_t s = rt.stream;
+    std::vector<cudaEvent_t> ev(static_cast<size_t>(3 * reps));
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    for (int it = 0; it < reps; ++it) {
+      CK(cudaMemcpyAsync(r->st.A.p, r->A0.p, r->A0.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      CK(cudaEventRecord(ev[3 * it], s));
+      factor_sweep(*r->fp, r->st, s, r->tables);
+      CK(cudaEventRecord(ev[3 * it + 1], s));
+      phase2_sweep(*r->p2, s, r->tables);
+      CK(cudaEventRecord(ev[3 * it + 2], s));
     }
-    std::vector<double> parts(static_cast<size_t>(m->layout.N) * fp->nb);
-    CK(cudaMemcpyAsync(parts.data(), st.logdet.p, parts.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
-    check_status(st.status, 1, m->layout, s);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    cudaEventDestroy(e2);
-    if (ms_per_rep) *ms_per_rep = total / reps;
+    CK(cudaEventSynchronize(ev.back()));
+    double total = 0;
+    float tf = 0, tp = 0;
+    for (int it = 0; it < reps; ++it) {
+      CK(cudaEventElapsedTime(&tf, ev[3 * it], ev[3 * it + 1]));
+      CK(cudaEventElapsedTime(&tp, ev[3 * it + 1], ev[3 * it + 2]));
+      total += tf + tp;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    std::vector<double> parts(r->fp->flow->host.logdet_doubles);
+    CK(cudaMemcpyAsync(parts.data(), r->st.logdet.p, parts.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    check_status(r->st.status, 1, r->layout, s);
+    r->logdet = reduce_logdet(parts.data(), r->layout.N, r->fp->nb);
+    if (ms_total) *ms_total = total;
     if (ms_factor) *ms_factor = tf;
     if (ms_phase2) *ms_phase2 = tp;
-    if (logdet) *logdet = reduce_logdet(parts.data(), m->layout.N, fp->nb);
   });
+}
+
+int tib_resident_info(tib_resident r, double* model, double* executed, double* logdet, long* launches) {
+  return guarded([&] {
+    need(r, "resident");
+    if (model) *model = r->model_flops;
+    if (executed) *executed = r->fp->flow->host.task_flops + r->p2->flow->host.task_flops;
+    if (logdet) *logdet = r->logdet;
+    if (launches) *launches = 2;  // one persistent dataflow kernel per sweep
+  });
+}
+
+int tib_resident_free(tib_resident r) {
+  delete r;
+  return kOk;
+}
+
+int tib_bench_resident(tib_matrix m, int device, int reps, int warmup, double* ms_per_rep, double* ms_factor,
+                       double* ms_phase2, double* logdet) {
+  tib_resident r = nullptr;
+  int st = tib_resident_create(m, device, &r);
+  if (st != kOk) return st;
+  double tot = 0;
+  if (warmup > 0) st = tib_resident_run(r, warmup, &tot, nullptr, nullptr);
+  if (st == kOk) st = tib_resident_run(r, reps, &tot, ms_factor, ms_phase2);
+  if (st == kOk) {
+    if (ms_per_rep) *ms_per_rep = tot / reps;
+    if (logdet) *logdet = r->logdet;
+  }
+  tib_resident_free(r);
+  return st;
 }
 
 }  // extern "C"

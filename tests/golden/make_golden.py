@@ -1,0 +1,99 @@
+"""Regenerates the golden fixtures in tests/golden/ from the REFERENCE itself.
+
+Run in the build container (it needs oracle/_ref, built from /root/reference by
+oracle/Makefile): python tests/golden/make_golden.py.  The GPU box never runs
+this; it only reads the committed fixtures.
+
+  kat.json        known-answer cases from the reference's own tests
+                  (test_smoke.py, test_selinv.cpp, test_cholesky.cpp) evaluated
+                  by the reference Python module
+  cases.npz       reference entries (r, c, value) for small generated cases
+                  over every selection kind (test_smoke.py / acceptance-4 style)
+  symbolic.json   reference factor pattern, closure, requested tiles and
+                  column work lists (ref_driver symbolic) per case
+  small.npz       diag(Sigma), logdet, trace of the SURVEY small config
+                  (n=10000 w=200 t=50 b=128 seed 42) from ref_driver dump
+"""
+import json
+import os
+import subprocess
+import sys
+import tempfile
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+REF = os.path.join(ROOT, "oracle", "_ref")
+sys.path.insert(0, os.path.join(REF, "py"))
+import tileinv as R  # noqa: E402  (the reference's pybind module)
+
+CASES = [
+    # n, w, t, density, seed, b, selection
+    (24, 5, 2, 0.8, 7, 4, "all"),
+    (24, 5, 2, 0.8, 7, 4, [(11, 2)]),
+    (30, 4, 1, 0.9, 3, 8, "diagonal"),
+    (60, 9, 3, 0.6, 11, 8, "pattern"),
+    (48, 8, 3, 0.5, 23, 8, "diagonal"),
+    (257, 30, 5, 0.7, 2, 32, "all"),
+    (300, 40, 7, 1.0, 3, 32, "pattern"),
+    (300, 40, 7, 1.0, 3, 32, [(299, 0), (150, 3), (5, 5), (200, 100), (5, 5)]),
+    (500, 60, 11, 0.3, 9, 120, "pattern"),
+    (700, 90, 12, 1.0, 5, 64, "diagonal"),
+    (1000, 150, 20, 1.0, 13, 128, "diagonal"),
+]
+
+
+def sel_arg(sel):
+    if isinstance(sel, str):
+        return sel
+    return ";".join(f"{r},{c}" for r, c in sel)
+
+
+def main():
+    kat = {}
+    a = np.array([[4.0, 2.0], [2.0, 5.0]])
+    kat["two_by_two_all"] = R.selected_inverse(R.from_dense(a), "all").entries()
+    kat["identity5_diag_b2"] = R.selected_inverse(R.from_dense(np.eye(5), tile_size=2), "diagonal").entries()
+    kat["diag_4_2_10_half"] = R.selected_inverse(R.from_dense(np.diag([4.0, 2.0, 10.0, 0.5]), tile_size=2),
+                                                 "diagonal").entries()
+    try:
+        R.factorize(R.from_dense(np.array([[1.0, 2.0], [2.0, 1.0]])))
+    except R.NotSpdError as e:
+        kat["not_spd_2x2"] = str(e)
+    d = np.eye(6)
+    d[4, 4] = -1.0
+    try:
+        R.factorize(R.from_dense(d, tile_size=2))
+    except R.NotSpdError as e:
+        kat["not_spd_pivot4"] = str(e)
+    with open(os.path.join(HERE, "kat.json"), "w") as f:
+        json.dump(kat, f, indent=1)
+
+    arrays, sym = {}, {}
+    for k, (n, w, t, dens, seed, b, sel) in enumerate(CASES):
+        m = R.generate(n, w, t, dens, seed=seed, tile_size=b)
+        res = R.selected_inverse(m, sel)
+        ent = np.array(res.entries(), dtype=np.float64).reshape(-1, 3)
+        arrays[f"case{k}"] = ent
+        out = subprocess.run([os.path.join(REF, "ref_driver"), "symbolic", str(n), str(w), str(t), str(b), str(seed),
+                              repr(dens), sel_arg(sel)], check=True, capture_output=True, text=True).stdout
+        sym[f"case{k}"] = {"args": [n, w, t, dens, seed, b, sel if isinstance(sel, str) else [list(p) for p in sel]],
+                           **json.loads(out)}
+    np.savez_compressed(os.path.join(HERE, "cases.npz"), **arrays)
+    with open(os.path.join(HERE, "symbolic.json"), "w") as f:
+        json.dump(sym, f)
+
+    with tempfile.TemporaryDirectory() as tmp:
+        out = subprocess.run([os.path.join(REF, "ref_driver"), "dump", "10000", "200", "50", "128", "42", "8",
+                              os.path.join(tmp, "small")], check=True, capture_output=True, text=True).stdout
+        info = json.loads(out)
+        diag = np.fromfile(os.path.join(tmp, "small.diag.f64"), dtype=np.float64)
+    np.savez_compressed(os.path.join(HERE, "small.npz"), diag=diag, logdet=info["logdet"], trace=info["trace"],
+                        gflop=info["gflop"], gflop_factorize=info["gflop_factorize"],
+                        gflop_phase1=info["gflop_phase1"], gflop_phase2=info["gflop_phase2"])
+    print("golden fixtures written:", sorted(os.listdir(HERE)))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,64 @@
+"""The device task plans, executed on the CPU by tests/plan_sim.py (numpy block
+products, in-order two-queue claiming), reproduce the oracle: this checks the
+dataflow decomposition, operand addressing, dependency counters and queue
+order without a GPU, and that the order is deadlock-free with one worker per
+queue."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import normwise
+from plan_sim import run_plans
+
+
+CASES = [
+    (700, 90, 12, 1.0, 5, 64, "pattern"),
+    (300, 40, 7, 1.0, 3, 32, "all"),
+    (520, 150, 20, 1.0, 11, 128, "pattern"),
+    (260, 60, 9, 0.4, 2, 128, "diagonal"),
+    (300, 40, 7, 1.0, 3, 32, [(299, 0), (150, 3), (5, 5), (200, 100)]),
+    (400, 0, 30, 1.0, 4, 64, "pattern"),       # no band: diagonal + arrow only
+    (1100, 300, 40, 1.0, 9, 256, "pattern"),   # bp = 256: 4x4 blocks per tile
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[str(c[:6]) for c in CASES])
+def test_plan_simulation_matches_oracle(tib, orc, case):
+    n, w, t, d, seed, b, sel = case
+    m = tib.generate(n, w, t, d, seed=seed, tile_size=b)
+    fpat, closure, sig, logdet, bad, var = run_plans(tib, m, sel)
+    ref = orc.selected_inverse_generated(n, w, t, d, seed, b, sel)
+    assert closure == ref["tiles"]
+    assert normwise(sig, ref["payload"]) <= 1e-12
+    assert abs(logdet - ref["logdet"]) <= 1e-12 * abs(ref["logdet"])
+    assert bad == np.iinfo(np.int64).max
+    if ref["diag"] is not None:
+        assert normwise(var, ref["diag"]) <= 1e-12
+
+
+def test_plan_simulation_fat_leaf(tib, orc, monkeypatch):
+    monkeypatch.setenv("TIB_FAT_LEAF", "1")
+    n, w, t, d, seed, b = 520, 150, 20, 1.0, 11, 128
+    m = tib.generate(n, w, t, d, seed=seed, tile_size=b)
+    _, _, sig, logdet, _, _ = run_plans(tib, m, "pattern")
+    ref = orc.selected_inverse_generated(n, w, t, d, seed, b, "pattern")
+    assert normwise(sig, ref["payload"]) <= 1e-12
+
+
+def test_plan_simulation_reports_not_spd(tib):
+    a = np.eye(6)
+    a[4, 4] = -1.0  # test_cholesky.cpp:161-182: pivot 4, tile (2, 2) at b = 2
+    m = tib.from_dense(a, tile_size=2)
+    *_, bad, _ = run_plans(tib, m, "pattern")
+    assert bad == 4
+
+
+def test_plans_are_topological_for_every_selection(tib):
+    # building a plan runs validate_dataflow (plan.cpp), which throws on any
+    # dependency not produced earlier in emission order
+    m = tib.generate(3000, 400, 60, 0.3, seed=1, tile_size=100)
+    for sel in ("pattern", "diagonal", "all", [(2999, 5), (10, 10)]):
+        for which in (0, 1):
+            p = tib.plan_export(m, sel, which, crit_workers=8)
+            assert len(p["tasks"]) > 0 and p["q0"] > 0
