@@ -219,6 +219,7 @@ struct DevPlan {
   DevArray<Seg> segs;
   DevArray<Dep> deps;
   DevArray<int> sigs;
+  DevArray<ZeroStrip> zero;
   GraphCache graphs;
   std::mutex mu;
 };
@@ -252,6 +253,7 @@ static std::shared_ptr<DevPlan> upload_plan(DataflowPlan&& host, int device, cud
   d->segs.upload(d->host.segs, s);
   d->deps.upload(d->host.deps, s);
   d->sigs.upload(d->host.sigs, s);
+  d->zero.upload(d->host.zero, s);
   CK(cudaStreamSynchronize(s));
   return d;
 }
@@ -334,16 +336,21 @@ static void write_trace(DevPlan& P, int batch, unsigned long long* d_trace, cuda
   const std::string path = std::string(trace_prefix()) + "." + std::to_string(g_trace_seq++) + ".bin";
   FILE* f = std::fopen(path.c_str(), "wb");
   if (!f) return;
-  const long long hdr[4] = {static_cast<long long>(P.host.tasks.size()), batch, P.host.q0.count, P.host.nb};
+  // v2: header, then the raw plan (tasks, deps, sigs, segs) so tools/trace_report.py
+  // can rebuild every dependency edge and walk the critical path
+  const long long hdr[8] = {-2,
+                            static_cast<long long>(P.host.tasks.size()),
+                            batch,
+                            P.host.q0.count,
+                            P.host.nb,
+                            static_cast<long long>(P.host.deps.size()),
+                            static_cast<long long>(P.host.sigs.size()),
+                            static_cast<long long>(P.host.segs.size())};
   std::fwrite(hdr, sizeof(hdr), 1, f);
-  std::vector<unsigned char> kinds(P.host.tasks.size());
-  std::vector<int> segc(P.host.tasks.size());
-  for (size_t i = 0; i < kinds.size(); ++i) {
-    kinds[i] = P.host.tasks[i].kind;
-    segc[i] = P.host.tasks[i].seg_count;
-  }
-  std::fwrite(kinds.data(), 1, kinds.size(), f);
-  std::fwrite(segc.data(), sizeof(int), segc.size(), f);
+  std::fwrite(P.host.tasks.data(), sizeof(DTask), P.host.tasks.size(), f);
+  std::fwrite(P.host.deps.data(), sizeof(Dep), P.host.deps.size(), f);
+  std::fwrite(P.host.sigs.data(), sizeof(int), P.host.sigs.size(), f);
+  std::fwrite(P.host.segs.data(), sizeof(Seg), P.host.segs.size(), f);
   std::fwrite(h.data(), 8, n, f);
   std::fclose(f);
 }
@@ -363,6 +370,7 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
     const size_t n = static_cast<size_t>(P.host.tasks.size()) * batch * 4;
     CK(cudaMallocAsync(reinterpret_cast<void**>(&d_trace), n * 8, s));
     CK(cudaMemsetAsync(d_trace, 0, n * 8, s));
+    launch_zero_strips(P.zero.p, static_cast<int>(P.zero.n), P.host.bp, batch, e.tables, s);
     launch_dataflow(P.tasks.p, P.segs.p, P.deps.p, P.sigs.p, P.host.q0, P.host.q1, batch, e.tables, e.claim, P.grid,
                     s, d_trace);
     CK(cudaGetLastError());
@@ -371,6 +379,7 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
     return;
   }
   auto enqueue = [&]() {
+    launch_zero_strips(P.zero.p, static_cast<int>(P.zero.n), P.host.bp, batch, e.tables, s);
     launch_dataflow(P.tasks.p, P.segs.p, P.deps.p, P.sigs.p, P.host.q0, P.host.q1, batch, e.tables, e.claim, P.grid,
                     s);
   };

@@ -19,6 +19,7 @@ int dataflow_grid(int device);
 void launch_dataflow(const DTask* tasks, const Seg* segs, const Dep* deps, const int* sigs, QueueDesc q0,
                      QueueDesc q1, int batch, const BaseTable* tables, int* claim, int grid, cudaStream_t s,
                      unsigned long long* trace = nullptr);
+void launch_zero_strips(const ZeroStrip* z, int count, int ld, int batch, const BaseTable* tables, cudaStream_t s);
 void launch_fill(double* p, double v, size_t count, cudaStream_t s);
 
 }  // namespace tib

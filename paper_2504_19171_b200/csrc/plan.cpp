@@ -172,7 +172,8 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
       t.diag_off = static_cast<long long>(j) * nb + kk;
       t.m0 = valid - kk * kB;
       t.n0 = static_cast<int>(static_cast<long>(j) * L.b + kk * kB);
-      t.seg_count = nb - 1 - kk;  // blocks to zero right of the diagonal block
+      t.seg_count = 0;
+      if (kk + 1 < nb) P.zero.push_back(ZeroStrip{blk_off(ds, bp, kk, kk) + kB, nb - 1 - kk, 0});
       t.ldc = t.ldc0 = bp;
       P.task_flops += 2.0 * (kB * kB * kB / 6.0) * 2;  // chol + inverse of the leaf
       if (fat) P.task_flops += 2.0 * kB * kB * kB * 2;

@@ -26,6 +26,10 @@ struct DataflowPlan {
   size_t scratch_doubles = 0; // per matrix
   size_t logdet_doubles = 0;  // per matrix
   double task_flops = 0;      // FLOPs actually executed by the block tasks (2 per FMA)
+  // 64-row strips right of each diagonal block that must read zero in the L and
+  // phase-1 stores (upper triangle of the diagonal tiles): origin offset and
+  // width in 64-column blocks; cleared by a separate kernel before the sweep.
+  std::vector<ZeroStrip> zero;
 };
 
 // Fused factorization + phase 1 over the FILLED pattern: per column, the

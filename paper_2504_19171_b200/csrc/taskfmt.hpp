@@ -81,6 +81,12 @@ struct Dep {
   int value;
 };
 
+// 64 rows x (blocks * 64) doubles at `off` in the L and phase-1 stores, zeroed.
+struct ZeroStrip {
+  long long off;
+  int blocks, pad;
+};
+
 // A queue is a contiguous range of the task array; `workers` CTAs serve q0
 // (the critical chain), the rest of the grid serves q1.
 struct QueueDesc {

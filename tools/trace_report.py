@@ -1,57 +1,150 @@
 """Summarise a dataflow task trace written with TIB_TRACE=<prefix> (engine.cpp
-write_trace): per queue busy / waiting time, per task-kind durations."""
+write_trace): per-queue busy / waiting time, per task-class durations, and the
+critical path -- walked back from the last task through the dependency whose
+counter was satisfied last (or, when the task was claimed after its inputs were
+ready, through the task that freed its CTA) -- broken down by task class."""
+import collections
 import sys
 
 import numpy as np
 
+DTASK = np.dtype({
+    "names": ["c_off", "c0_off", "cm_off", "diag_off", "ldc", "ldc0", "m0", "n0", "seg_begin", "seg_count",
+              "dep_begin", "sig_begin", "dep_count", "sig_count", "kind", "mode", "c_store", "c0_store",
+              "cm_store", "diag_store"],
+    "formats": ["<i8"] * 4 + ["<i4"] * 8 + ["<u2"] * 2 + ["u1"] * 6,
+    "offsets": [0, 8, 16, 24, 32, 36, 40, 44, 48, 52, 56, 60, 64, 66, 68, 69, 70, 71, 72, 73],
+    "itemsize": 80,
+})
+DEP = np.dtype([("counter", "<i4"), ("value", "<i4")])
+SEG = np.dtype({
+    "names": ["a_off", "b_off", "lda", "ldb", "k_lo", "k_hi", "flags", "a_store", "b_store"],
+    "formats": ["<i8", "<i8", "<i4", "<i4", "<i2", "<i2", "u1", "u1", "u1"],
+    "offsets": [0, 8, 16, 20, 24, 26, 28, 29, 30],
+    "itemsize": 32,
+})
+STORE = {0: "A", 1: "L", 2: "P1", 3: "S", 5: "T", 255: "-"}
+
 
 def load(path):
     with open(path, "rb") as f:
-        hdr = np.frombuffer(f.read(32), np.int64)
-        ntask, batch, nq0, nb = (int(x) for x in hdr)
-        kinds = np.frombuffer(f.read(ntask), np.uint8)
-        segc = np.frombuffer(f.read(4 * ntask), np.int32)
+        hdr = np.frombuffer(f.read(64), np.int64)
+        if hdr[0] != -2:
+            raise SystemExit(f"{path}: old trace format")
+        ntask, batch, nq0, nb, ndep, nsig, nseg = (int(x) for x in hdr[1:])
+        tasks = np.frombuffer(f.read(80 * ntask), DTASK)
+        deps = np.frombuffer(f.read(8 * ndep), DEP)
+        sigs = np.frombuffer(f.read(4 * nsig), np.int32)
+        segs = np.frombuffer(f.read(32 * nseg), SEG)
         rec = np.frombuffer(f.read(), np.uint64).reshape(-1, 4)
-    return ntask, batch, nq0, nb, kinds, segc, rec
+    return dict(ntask=ntask, batch=batch, nq0=nq0, nb=nb, tasks=tasks, deps=deps, sigs=sigs, segs=segs, rec=rec)
+
+
+def label(t, q0):
+    if t["kind"] == 1:
+        return "leaf" + ("+fat" if t["mode"] & 2 else "")
+    cs, c0 = STORE.get(int(t["c_store"]), "?"), STORE.get(int(t["c0_store"]), "?")
+    q = "q0" if q0 else "q1"
+    name = {("q0", "L"): "paneld", ("q0", "A"): "traild", ("q0", "T"): "trow", ("q0", "P1"): "xrow",
+            ("q1", "L"): "panel", ("q1", "A"): "update", ("q1", "P1"): "W"}.get((q, cs))
+    if name is None:
+        if cs == "S":
+            name = {0: "off", 1: "symdiag", 2: "mirror"}[int(t["mode"])] + ("+c0" if c0 == "S" else "")
+        else:
+            name = f"{cs}"
+    return f"{q}:{name}/s{int(t['seg_count'])}"
 
 
 def report(path):
-    ntask, batch, nq0, nb, kinds, segc, rec = load(path)
+    d = load(path)
+    tasks, deps, sigs, rec, batch, nq0 = d["tasks"], d["deps"], d["sigs"], d["rec"], d["batch"], d["nq0"]
     ok = rec[:, 2] > 0
     rec = rec[ok]
-    claim, ready, done = (rec[:, i].astype(np.float64) for i in range(3))
-    task = (rec[:, 3] >> 32).astype(np.int64)
+    claim, ready, done = (rec[:, i].astype(np.float64) / 1e3 for i in range(3))  # us
+    tidx = (rec[:, 3] >> 32).astype(np.int64)
+    mat = ((rec[:, 3] >> 16) & 0xFFFF).astype(np.int64)
     sm = (rec[:, 3] & 0xFFFF).astype(np.int64)
     t0 = claim.min()
-    span = (done.max() - t0) / 1e3
-    q0 = task < nq0
-    print(f"{path}: tasks={len(rec)} (q0 {q0.sum()}, q1 {(~q0).sum()}) span={span:.1f} us")
+    claim, ready, done = claim - t0, ready - t0, done - t0
+    span = done.max()
+    q0 = tidx < nq0
+    labels = np.array([label(tasks[i], i < nq0) for i in range(len(tasks))])
+    lab = labels[tidx]
+    print(f"{path}: tasks={len(rec)} (q0 {q0.sum()}, q1 {(~q0).sum()}) batch={batch} span={span:.1f} us")
+    nsm = len(np.unique(sm))
+    busy_all = (done - ready).sum()
+    print(f"  CTA-busy fraction {busy_all / (span * 2 * nsm):.3f} (2 CTAs x {nsm} SMs)")
     for name, m in (("q0/crit", q0), ("q1/bulk", ~q0)):
         if m.sum() == 0:
             continue
-        wait = (ready[m] - claim[m]).sum() / 1e3
-        busy = (done[m] - ready[m]).sum() / 1e3
-        workers = len(np.unique(sm[m]))
+        wait = (ready[m] - claim[m]).sum()
+        busy = (done[m] - ready[m]).sum()
         print(f"  {name}: busy {busy:.0f} us, waiting {wait:.0f} us (wait share {wait / (wait + busy):.2f}), "
-              f"SMs {workers}, first {(claim[m].min() - t0) / 1e3:.1f} last-done {(done[m].max() - t0) / 1e3:.1f} us")
-    dur = (done - ready) / 1e3
-    k = kinds[task]
-    s = segc[task]
-    print("  leaf tasks: n=%d mean %.1f us  p50 %.1f  max %.1f" % ((k == 1).sum(), dur[k == 1].mean() if (k == 1).any() else 0,
-          np.median(dur[k == 1]) if (k == 1).any() else 0, dur[k == 1].max() if (k == 1).any() else 0))
-    for sc in sorted(set(s[(k == 0)].tolist())):
-        m = (k == 0) & (s == sc)
-        for name, qm in (("q0", q0), ("q1", ~q0)):
-            mm = m & qm
-            if mm.sum():
-                print(f"  gemm seg_count={sc} {name}: n={mm.sum()} mean {dur[mm].mean():.1f} us p50 {np.median(dur[mm]):.1f}")
-    # utilisation timeline (10 buckets)
-    edges = np.linspace(t0, done.max(), 11)
+              f"SMs {len(np.unique(sm[m]))}, last-done {done[m].max():.1f} us")
+    dur = done - ready
+    print("  per class: n, mean us, p50, total ms")
+    for L in sorted(set(lab.tolist())):
+        m = lab == L
+        print(f"    {L:28s} n={m.sum():6d} mean {dur[m].mean():7.1f} p50 {np.median(dur[m]):7.1f} total {dur[m].sum() / 1e3:8.1f}")
+    edges = np.linspace(0, span, 11)
     busy_t = []
     for a, b in zip(edges[:-1], edges[1:]):
         ov = np.clip(np.minimum(done, b) - np.maximum(ready, a), 0, None).sum()
-        busy_t.append(ov / ((b - a) * 2 * len(np.unique(sm))) if b > a else 0)
+        busy_t.append(ov / ((b - a) * 2 * nsm))
     print("  busy fraction per tenth of the sweep:", " ".join(f"{x:.2f}" for x in busy_t))
+
+    # ---- critical path
+    key = {(int(t), int(mm)): r for r, (t, mm) in enumerate(zip(tidx, mat))}
+    events = collections.defaultdict(list)  # (counter, mat) -> [(done, rec)]
+    for r in range(len(rec)):
+        t = tasks[tidx[r]]
+        for s in range(t["sig_begin"], t["sig_begin"] + t["sig_count"]):
+            events[(int(sigs[s]), int(mat[r]))].append((done[r], r))
+    for v in events.values():
+        v.sort()
+    by_sm = collections.defaultdict(list)
+    for r in np.argsort(done):
+        by_sm[int(sm[r])].append(r)
+    sm_done = {s: np.array([done[r] for r in rs]) for s, rs in by_sm.items()}
+    r = int(np.argmax(done))
+    path_exec = collections.Counter()
+    path_n = collections.Counter()
+    gap_dep = gap_claim = 0.0
+    steps = 0
+    while r is not None and steps < 10 ** 7:
+        steps += 1
+        t = tasks[tidx[r]]
+        path_exec[lab[r]] += done[r] - ready[r]
+        path_n[lab[r]] += 1
+        best, bt = None, -1.0
+        for k in range(t["dep_begin"], t["dep_begin"] + t["dep_count"]):
+            dp = deps[k]
+            ev = events.get((int(dp["counter"]), int(mat[r])), [])
+            if dp["value"] <= 0 or len(ev) < dp["value"]:
+                continue
+            tm, pr = ev[dp["value"] - 1]
+            if tm > bt:
+                best, bt = pr, tm
+        if best is not None and bt >= claim[r] - 0.5:
+            gap_dep += max(0.0, ready[r] - bt)
+            r = best
+            continue
+        # claimed late: follow the task that freed a CTA on this SM
+        gap_dep += max(0.0, ready[r] - max(bt, claim[r]))
+        arr = sm_done[int(sm[r])]
+        i = np.searchsorted(arr, claim[r] + 1e-3) - 1
+        if i < 0:
+            break
+        prev = by_sm[int(sm[r])][i]
+        gap_claim += max(0.0, claim[r] - done[prev])
+        path_exec["(claim-wait)"] += 0
+        r = prev if prev != r else None
+    tot = sum(path_exec.values())
+    print(f"  critical path: {sum(path_n.values())} tasks, exec {tot / 1e3:.1f} ms, dep-latency {gap_dep / 1e3:.1f} ms, "
+          f"claim gaps {gap_claim / 1e3:.1f} ms (span {span / 1e3:.1f} ms)")
+    for L, v in path_exec.most_common():
+        if path_n[L]:
+            print(f"    {L:28s} n={path_n[L]:6d} exec {v / 1e3:8.2f} ms  mean {v / path_n[L]:6.1f} us")
 
 
 if __name__ == "__main__":
