@@ -7,7 +7,7 @@
 #include <vector>
 using namespace tib;
 
-template <bool F>
+template <bool F, bool WX = true, bool BK = true>
 __global__ void chol_kernel(const double* A, double* out, long long* cyc, int reps) {
   extern __shared__ __align__(16) double smem[];
   double* SA = smem;
@@ -17,7 +17,7 @@ __global__ void chol_kernel(const double* A, double* out, long long* cyc, int re
   __syncthreads();
   long long t0 = clock64();
   for (int r = 0; r < reps; ++r) {
-    if (threadIdx.x < 32) chol32_warp<F>(SA, SX, vec, vec + 128, vec + 256);
+    if (threadIdx.x < 32) chol32_warp<F, WX, BK>(SA, SX, vec, vec + 128, vec + 256);
     __syncthreads();
   }
   long long t1 = clock64();
@@ -82,6 +82,18 @@ int main() {
       cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
       printf("{\"chol32_inverse_only_cycles\": %lld, \"threads\": %d}\n", c, threads);
     }
+  }
+  cudaFuncSetAttribute(chol_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFlowSmemBytes);
+  for (int it = 0; it < 2; ++it) {
+    chol_kernel<true, false><<<1, 32, kFlowSmemBytes>>>(dA32, dout, cyc, 20);
+    cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("{\"chol32_factor_noX_cycles\": %lld}\n", c);
+  }
+  cudaFuncSetAttribute(chol_kernel<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFlowSmemBytes);
+  for (int it = 0; it < 2; ++it) {
+    chol_kernel<true, false, false><<<1, 32, kFlowSmemBytes>>>(dA32, dout, cyc, 20);
+    cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("{\"chol32_chain_only_cycles\": %lld}\n", c);
   }
   cudaFuncSetAttribute(chol2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFlowSmemBytes);
   for (int mode : {0, 1, 0, 1}) {
