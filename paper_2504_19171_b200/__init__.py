@@ -442,12 +442,12 @@ __all__ = [
 # ---- dataflow plan inspection (host only) and resident timing sessions --------
 
 DTASK_DTYPE = np.dtype({
-    "names": ["c_off", "c0_off", "cm_off", "diag_off", "ldc", "ldc0", "m0", "n0", "seg_begin", "seg_count",
-              "dep_begin", "sig_begin", "dep_count", "sig_count", "kind", "mode", "c_store", "c0_store",
-              "cm_store", "diag_store"],
-    "formats": ["<i8"] * 4 + ["<i4"] * 8 + ["<u2"] * 2 + ["u1"] * 6,
-    "offsets": [0, 8, 16, 24, 32, 36, 40, 44, 48, 52, 56, 60, 64, 66, 68, 69, 70, 71, 72, 73],
-    "itemsize": 80,
+    "names": ["c_off", "c0_off", "cm_off", "diag_off", "p_off", "ldc", "ldc0", "m0", "n0", "seg_begin", "seg_count",
+              "dep_begin", "sig_begin", "aux0", "aux1", "dep_count", "sig_count", "kind", "mode", "c_store",
+              "c0_store", "cm_store", "diag_store", "dep2_count"],
+    "formats": ["<i8"] * 5 + ["<i4"] * 10 + ["<u2"] * 2 + ["u1"] * 7,
+    "offsets": [0, 8, 16, 24, 32, 40, 44, 48, 52, 56, 60, 64, 68, 72, 76, 80, 82, 84, 85, 86, 87, 88, 89, 90],
+    "itemsize": 96,
 })
 SEG_DTYPE = np.dtype({
     "names": ["a_off", "b_off", "lda", "ldb", "k_lo", "k_hi", "flags", "a_store", "b_store"],

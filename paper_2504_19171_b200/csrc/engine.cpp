@@ -193,20 +193,20 @@ struct GraphCache {
   struct Entry {
     cudaGraphExec_t exec = nullptr;
     BaseTable* tables = nullptr;  // device copy of the per-matrix base tables, owned here
-    int* claim = nullptr;         // queue claim counters
+    int* sched = nullptr;         // scheduler state: ctl[128], missing[batch x T], slots0, slots1
   };
   std::map<int, Entry> by_batch;
-  Entry& get(int batch) {
+  Entry& get(int batch, size_t ntasks) {
     Entry& e = by_batch[batch];
     if (!e.tables) CK(cudaMalloc(reinterpret_cast<void**>(&e.tables), sizeof(BaseTable) * batch));
-    if (!e.claim) CK(cudaMalloc(reinterpret_cast<void**>(&e.claim), 2 * sizeof(int)));
+    if (!e.sched) CK(cudaMalloc(reinterpret_cast<void**>(&e.sched), (128 + 256 + 2 * ntasks * batch) * sizeof(int)));
     return e;
   }
   ~GraphCache() {
     for (auto& kv : by_batch) {
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
       if (kv.second.tables) cudaFree(kv.second.tables);
-      if (kv.second.claim) cudaFree(kv.second.claim);
+      if (kv.second.sched) cudaFree(kv.second.sched);
     }
   }
 };
@@ -220,6 +220,8 @@ struct DevPlan {
   DevArray<Dep> deps;
   DevArray<int> sigs;
   DevArray<ZeroStrip> zero;
+  DevArray<int> need, vbase, vidx, wl, init0, init1;
+  DevArray<DTask> chain;
   GraphCache graphs;
   std::mutex mu;
 };
@@ -241,7 +243,7 @@ static int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e && *e ? std::atoi(e) : dflt;
 }
-static int crit_workers() { return env_int("TIB_CRIT_WORKERS", 16); }
+static int crit_workers() { return env_int("TIB_CRIT_WORKERS", 4); }
 
 static std::shared_ptr<DevPlan> upload_plan(DataflowPlan&& host, int device, cudaStream_t s) {
   auto d = std::make_shared<DevPlan>();
@@ -254,6 +256,13 @@ static std::shared_ptr<DevPlan> upload_plan(DataflowPlan&& host, int device, cud
   d->deps.upload(d->host.deps, s);
   d->sigs.upload(d->host.sigs, s);
   d->zero.upload(d->host.zero, s);
+  d->need.upload(d->host.need, s);
+  d->vbase.upload(d->host.vbase, s);
+  d->vidx.upload(d->host.vidx, s);
+  d->wl.upload(d->host.wl, s);
+  d->init0.upload(d->host.init0, s);
+  d->init1.upload(d->host.init1, s);
+  d->chain.upload(d->host.chain, s);
   CK(cudaStreamSynchronize(s));
   return d;
 }
@@ -283,7 +292,7 @@ static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int 
   plan->sym = symbolic_cholesky(pattern);
   plan->L = plan->sym.filled.layout();
   plan->flow = upload_plan(build_factor_dataflow(plan->sym.filled, crit_workers(), env_int("TIB_DEFER_W", 2),
-                                                  env_int("TIB_FAT_LEAF", 0) != 0),
+                                                  env_int("TIB_FAT_LEAF", 0) != 0, env_int("TIB_CHAIN", 1) != 0),
                            device, s);
   plan->bp = plan->flow->host.bp;
   plan->nb = plan->flow->host.nb;
@@ -338,19 +347,22 @@ static void write_trace(DevPlan& P, int batch, unsigned long long* d_trace, cuda
   if (!f) return;
   // v2: header, then the raw plan (tasks, deps, sigs, segs) so tools/trace_report.py
   // can rebuild every dependency edge and walk the critical path
-  const long long hdr[8] = {-2,
+  const long long hdr[10] = {-3,
                             static_cast<long long>(P.host.tasks.size()),
                             batch,
                             P.host.q0.count,
                             P.host.nb,
                             static_cast<long long>(P.host.deps.size()),
                             static_cast<long long>(P.host.sigs.size()),
-                            static_cast<long long>(P.host.segs.size())};
+                            static_cast<long long>(P.host.segs.size()),
+                            static_cast<long long>(P.host.slot_tiles.size()),
+                            P.host.bp};
   std::fwrite(hdr, sizeof(hdr), 1, f);
   std::fwrite(P.host.tasks.data(), sizeof(DTask), P.host.tasks.size(), f);
   std::fwrite(P.host.deps.data(), sizeof(Dep), P.host.deps.size(), f);
   std::fwrite(P.host.sigs.data(), sizeof(int), P.host.sigs.size(), f);
   std::fwrite(P.host.segs.data(), sizeof(Seg), P.host.segs.size(), f);
+  std::fwrite(P.host.slot_tiles.data(), sizeof(Coord), P.host.slot_tiles.size(), f);
   std::fwrite(h.data(), 8, n, f);
   std::fclose(f);
 }
@@ -361,28 +373,48 @@ static void write_trace(DevPlan& P, int batch, unsigned long long* d_trace, cuda
 static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStream_t s) {
   std::lock_guard<std::mutex> lk(P.mu);
   const int batch = static_cast<int>(tables.size());
-  GraphCache::Entry& e = P.graphs.get(batch);
+  const size_t nt = P.host.tasks.size();
+  GraphCache::Entry& e = P.graphs.get(batch, nt);
   CK(cudaMemcpyAsync(e.tables, tables.data(), sizeof(BaseTable) * batch, cudaMemcpyHostToDevice, s));
   for (const BaseTable& t : tables)
     CK(cudaMemsetAsync(t.p[kStoreCounters], 0, static_cast<size_t>(P.host.counters) * sizeof(int), s));
+  FlowArgs a{};
+  a.tasks = P.tasks.p;
+  a.segs = P.segs.p;
+  a.deps = P.deps.p;
+  a.sigs = P.sigs.p;
+  a.vbase = P.vbase.p;
+  a.vidx = P.vidx.p;
+  a.wl = P.wl.p;
+  a.q0 = P.host.q0;
+  a.q1 = P.host.q1;
+  a.batch = batch;
+  a.ntasks = static_cast<int>(nt);
+  a.tables = e.tables;
+  a.ctl = e.sched;
+  a.sm_flags = e.sched + 128;
+  a.missing = e.sched + 128 + 256;
+  a.chain = P.chain.p;
+  a.dedicate = batch <= env_int("TIB_DEDICATE_MAX_BATCH", 4) ? 1 : 0;
+  a.slots0 = a.missing + nt * batch;
+  a.slots1 = a.slots0 + static_cast<size_t>(P.host.q0.count) * batch;
+  a.trace = nullptr;
+  auto enqueue = [&]() {
+    launch_zero_strips(P.zero.p, static_cast<int>(P.zero.n), P.host.bp, batch, e.tables, s);
+    launch_dataflow(a, P.need.p, P.init0.p, static_cast<int>(P.init0.n), P.init1.p, static_cast<int>(P.init1.n), P.grid, s);
+  };
   if (trace_prefix()) {
     unsigned long long* d_trace = nullptr;
-    const size_t n = static_cast<size_t>(P.host.tasks.size()) * batch * 4;
+    const size_t n = nt * batch * 4;
     CK(cudaMallocAsync(reinterpret_cast<void**>(&d_trace), n * 8, s));
     CK(cudaMemsetAsync(d_trace, 0, n * 8, s));
-    launch_zero_strips(P.zero.p, static_cast<int>(P.zero.n), P.host.bp, batch, e.tables, s);
-    launch_dataflow(P.tasks.p, P.segs.p, P.deps.p, P.sigs.p, P.host.q0, P.host.q1, batch, e.tables, e.claim, P.grid,
-                    s, d_trace);
+    a.trace = d_trace;
+    enqueue();
     CK(cudaGetLastError());
     write_trace(P, batch, d_trace, s);
     CK(cudaFreeAsync(d_trace, s));
     return;
   }
-  auto enqueue = [&]() {
-    launch_zero_strips(P.zero.p, static_cast<int>(P.zero.n), P.host.bp, batch, e.tables, s);
-    launch_dataflow(P.tasks.p, P.segs.p, P.deps.p, P.sigs.p, P.host.q0, P.host.q1, batch, e.tables, e.claim, P.grid,
-                    s);
-  };
   if (!use_graphs()) {
     enqueue();
     CK(cudaGetLastError());

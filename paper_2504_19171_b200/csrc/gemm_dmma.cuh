@@ -133,9 +133,10 @@ struct LocalSegs {
   __device__ __forceinline__ RSeg get(int i) const { return segs[i]; }
 };
 
-// Runs one task on the calling CTA (kGemmThreads threads).  smem must hold
-// kGemmSmemBytes.  Safe to call repeatedly from a persistent loop: it ends
-// with a __syncthreads so the ring can be reused.
+// Main loop of one task on the calling CTA (kGemmThreads threads): the block
+// product sum_s sign_s op(A_s) op(B_s) into acc (the warp's 32 x 32 patch as
+// 4 x 4 m8n8 fragments).  smem must hold kGemmSmemBytes; ends with the ring
+// drained (no barrier: the epilogue does not touch shared memory).
 //
 // Inner loop: the two shared layouts differ only in strides, so fragment
 // addresses are (stage base) + k*sK + row*sM with per-stage strides -- no
@@ -144,13 +145,12 @@ struct LocalSegs {
 // when the sign changes between chunks (at most a couple of times per task)
 // instead of per fragment.
 template <class Src>
-__device__ __forceinline__ void gemm_task(const RTask& t, const Src& src, double* smem) {
+__device__ __forceinline__ void gemm_mainloop(const RTask& t, const Src& src, double* smem, double (&acc)[4][4][2]) {
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   const int fr = lane >> 2, fc = lane & 3;
 
-  double acc[4][4][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -260,13 +260,27 @@ __device__ __forceinline__ void gemm_task(const RTask& t, const Src& src, double
         acc[i][j][1] = -acc[i][j][1];
       }
   }
+  __syncthreads();  // every warp is done with the ring before the next task refills it
+}
 
-  // Epilogue: C = C0 + acc.
+// Position of fragment (i, j, h) of the calling thread in the 64 x 64 block.
+__device__ __forceinline__ int frag_row(int i) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  return (warp >> 1) * 32 + i * 8 + (lane >> 2);
+}
+__device__ __forceinline__ int frag_col(int j) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  return (warp & 1) * 32 + j * 8 + (lane & 3) * 2;
+}
+
+// Epilogue: C = C0 + acc, written per mode; ends with a barrier so thread 0
+// may release the task's signals.
+__device__ __forceinline__ void gemm_epilogue(const RTask& t, const double (&acc)[4][4][2]) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int r = wm + i * 8 + fr, c = wn + j * 8 + fc * 2;
+      const int r = frag_row(i), c = frag_col(j);
       double v0 = acc[i][j][0], v1 = acc[i][j][1];
       if (t.C0) {
         const double2 o = __ldcg(reinterpret_cast<const double2*>(t.C0 + static_cast<size_t>(r) * t.ldc0 + c));
@@ -294,6 +308,40 @@ __device__ __forceinline__ void gemm_task(const RTask& t, const Src& src, double
     }
   }
   __syncthreads();
+}
+
+// Split-K: a part's accumulators -> its 64 x 64 scratch slot (row-major).
+__device__ __forceinline__ void split_store(double* slot, const double (&acc)[4][4][2]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      __stcg(reinterpret_cast<double2*>(slot + frag_row(i) * kBN + frag_col(j)), make_double2(acc[i][j][0], acc[i][j][1]));
+}
+
+// Reducer: acc = P_0 + P_1 + ... + P_{parts-1} in part order, every part read
+// back from its slot (the caller's own included, bitwise what it stored), so
+// the result does not depend on which part arrived last.
+__device__ __forceinline__ void split_reduce(const double* slots, int parts, double (&acc)[4][4][2]) {
+  for (int p = 0; p < parts; ++p) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double2 v =
+            __ldcg(reinterpret_cast<const double2*>(slots + static_cast<size_t>(p) * kBM * kBN + frag_row(i) * kBN + frag_col(j)));
+        acc[i][j][0] = p == 0 ? v.x : acc[i][j][0] + v.x;
+        acc[i][j][1] = p == 0 ? v.y : acc[i][j][1] + v.y;
+      }
+  }
+}
+
+// One plain task: main loop + epilogue.
+template <class Src>
+__device__ __forceinline__ void gemm_task(const RTask& t, const Src& src, double* smem) {
+  double acc[4][4][2];
+  gemm_mainloop(t, src, smem, acc);
+  gemm_epilogue(t, acc);
 }
 
 __device__ __forceinline__ RTask resolve_task(const Task& s, const BaseTable& bt) {

@@ -16,9 +16,31 @@ struct DevStatus {
 
 int configure_kernels();  // smem attribute; returns cudaError_t
 int dataflow_grid(int device);
-void launch_dataflow(const DTask* tasks, const Seg* segs, const Dep* deps, const int* sigs, QueueDesc q0,
-                     QueueDesc q1, int batch, const BaseTable* tables, int* claim, int grid, cudaStream_t s,
-                     unsigned long long* trace = nullptr);
+// Everything the persistent sweep kernel reads: the plan (device copies),
+// the per-matrix base tables, and the per-sweep scheduler state.
+struct FlowArgs {
+  const DTask* tasks;
+  const Seg* segs;
+  const Dep* deps;
+  const int* sigs;
+  const int* vbase;  // counters + 1
+  const int* vidx;
+  const int* wl;
+  QueueDesc q0, q1;
+  int batch, ntasks;
+  const BaseTable* tables;
+  int* missing;  // batch x ntasks
+  int* slots0;   // q0.count x batch
+  int* slots1;   // q1.count x batch
+  int* ctl;      // head0, tail0, head1, tail1 (128-byte apart)
+  const DTask* chain;  // chain steps (kChainTask)
+  int* sm_flags;       // [256]: SM hosts a running chain
+  int dedicate;        // chains get their SM to themselves
+  unsigned long long* trace;
+};
+
+void launch_dataflow(const FlowArgs& a, const int* need, const int* init0, int n_init0, const int* init1, int n_init1,
+                     int grid, cudaStream_t s);
 void launch_zero_strips(const ZeroStrip* z, int count, int ld, int batch, const BaseTable* tables, cudaStream_t s);
 void launch_fill(double* p, double v, size_t count, cudaStream_t s);
 

@@ -22,11 +22,13 @@ struct Builder {
   std::vector<unsigned char> queue;
   explicit Builder(DataflowPlan& p) : P(p) {}
 
-  DTask& add(int q, const std::vector<Dep>& deps, const std::vector<int>& sigs) {
+  DTask& add(int q, const std::vector<Dep>& deps, const std::vector<int>& sigs, const std::vector<Dep>& deps2 = {}) {
     DTask t{};
     t.dep_begin = static_cast<int>(P.deps.size());
     t.dep_count = static_cast<unsigned short>(deps.size());
+    t.dep2_count = static_cast<unsigned char>(deps2.size());
     P.deps.insert(P.deps.end(), deps.begin(), deps.end());
+    P.deps.insert(P.deps.end(), deps2.begin(), deps2.end());
     t.sig_begin = static_cast<int>(P.sigs.size());
     t.sig_count = static_cast<unsigned short>(sigs.size());
     P.sigs.insert(P.sigs.end(), sigs.begin(), sigs.end());
@@ -54,7 +56,39 @@ struct Builder {
   }
   // Splits the emission order into the two queues; returns the global order
   // expressed in final task indices.
-  std::vector<int> finish(int crit_workers) {
+  std::vector<int> finish(int crit_workers, bool chain = false) {
+    // dependency check in emission order (before any restructuring)
+    P.tasks = all;
+    std::vector<int> ident(all.size());
+    for (size_t i = 0; i < all.size(); ++i) ident[i] = static_cast<int>(i);
+    validate_dataflow(P, ident);
+    if (chain) {
+      // the leaves become chain steps, in emission order (one persistent task runs them)
+      std::vector<DTask> rest;
+      std::vector<unsigned char> rq;
+      P.chain.clear();
+      for (size_t i = 0; i < all.size(); ++i) {
+        if (all[i].kind == kLeafTask) {
+          P.chain.push_back(all[i]);
+        } else {
+          rest.push_back(all[i]);
+          rq.push_back(queue[i]);
+        }
+      }
+      DTask c{};
+      c.kind = kChainTask;
+      c.c_store = c.c0_store = c.cm_store = c.diag_store = kStoreNone;
+      c.seg_begin = 0;
+      c.seg_count = static_cast<int>(P.chain.size());
+      all.clear();
+      queue.clear();
+      if (!P.chain.empty()) {
+        all.push_back(c);
+        queue.push_back(0);
+      }
+      all.insert(all.end(), rest.begin(), rest.end());
+      queue.insert(queue.end(), rq.begin(), rq.end());
+    }
     std::vector<int> pos(all.size());
     P.tasks.clear();
     P.tasks.reserve(all.size());
@@ -71,7 +105,43 @@ struct Builder {
       }
     P.q0 = QueueDesc{0, n0, n0 > 0 ? crit_workers : 0, 0};
     P.q1 = QueueDesc{n0, static_cast<int>(P.tasks.size()) - n0, 0, 0};
+    finalize_waiters();
     return pos;
+  }
+  void finalize_waiters() {
+    const size_t nt = P.tasks.size();
+    const size_t nc = static_cast<size_t>(P.counters);
+    P.need.assign(nt, 0);
+    std::vector<int> maxv(nc, 0);
+    std::vector<std::pair<long long, int>> w;  // ((counter << 32) | value, task)
+    for (size_t t = 0; t < nt; ++t) {
+      const DTask& k = P.tasks[t];
+      for (int d = k.dep_begin; d < k.dep_begin + k.dep_count; ++d) {
+        const Dep& dp = P.deps[static_cast<size_t>(d)];
+        if (dp.value <= 0) continue;
+        ++P.need[t];
+        maxv[static_cast<size_t>(dp.counter)] = std::max(maxv[static_cast<size_t>(dp.counter)], dp.value);
+        w.push_back({(static_cast<long long>(dp.counter) << 32) | dp.value, static_cast<int>(t)});
+      }
+    }
+    std::stable_sort(w.begin(), w.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+    P.wl.resize(w.size());
+    for (size_t i = 0; i < w.size(); ++i) P.wl[i] = w[i].second;
+    P.vbase.assign(nc + 1, 0);
+    for (size_t c = 0; c < nc; ++c) P.vbase[c + 1] = P.vbase[c] + maxv[c] + 2;
+    P.vidx.assign(static_cast<size_t>(P.vbase[nc]), 0);
+    size_t pos = 0;
+    for (size_t c = 0; c < nc; ++c) {
+      for (int v = 0; v <= maxv[c] + 1; ++v) {
+        const long long key = (static_cast<long long>(c) << 32) | v;
+        while (pos < w.size() && w[pos].first < key) ++pos;
+        P.vidx[static_cast<size_t>(P.vbase[c] + v)] = static_cast<int>(pos);
+      }
+    }
+    P.init0.clear();
+    P.init1.clear();
+    for (size_t t = 0; t < nt; ++t)
+      if (P.need[t] == 0) (static_cast<int>(t) < P.q0.count ? P.init0 : P.init1).push_back(static_cast<int>(t));
   }
 };
 
@@ -86,18 +156,22 @@ void validate_dataflow(const DataflowPlan& plan, const std::vector<int>& order) 
   std::vector<int> cnt(static_cast<size_t>(plan.counters), 0);
   for (int ti : order) {
     const DTask& t = plan.tasks[static_cast<size_t>(ti)];
-    for (int d = t.dep_begin; d < t.dep_begin + t.dep_count; ++d) {
+    for (int d = t.dep_begin; d < t.dep_begin + t.dep_count + t.dep2_count; ++d) {
       const Dep& dp = plan.deps[static_cast<size_t>(d)];
       if (dp.counter < 0 || dp.counter >= plan.counters || cnt[static_cast<size_t>(dp.counter)] < dp.value)
         throw Error(kErrConsistency, "dataflow plan: task " + std::to_string(ti) + " depends on counter " +
                                          std::to_string(dp.counter) + " >= " + std::to_string(dp.value) +
                                          " not produced earlier in emission order");
     }
+    // a split group signals once, through its reducer (the last part to arrive;
+    // in emission order, the last part)
+    if (t.kind == kSplitTask && (t.aux1 >> 8) != (t.aux1 & 255) - 1) continue;
     for (int s = t.sig_begin; s < t.sig_begin + t.sig_count; ++s) ++cnt[static_cast<size_t>(plan.sigs[static_cast<size_t>(s)])];
   }
 }
 
-DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer_w, bool fat_leaf) {
+DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer_w, bool fat_leaf, bool chain) {
+  if (chain) fat_leaf = true;
   DataflowPlan P;
   P.L = F.layout();
   const Layout& L = P.L;
@@ -106,12 +180,25 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
   P.nb = nb;
   const long T = static_cast<long>(F.size());
   const int N = L.N;
+  // split-K shapes of the critical tail (see below)
+  auto panel_parts = [&](int q) { return (q + 1) * kB > 256 ? (q + 2) / 2 : 1; };  // K = 64 (q+1), parts of <= 128
+  const int upd_parts = nb > 2 ? (nb + 1) / 2 : 1;                                // K = bp, parts of 128
+  // per column: the progressive panels of the first two off-diagonal tiles and
+  // the split updates of tiles (k0, k0) and (k1, k0)
+  int panel_slots = 0;
+  for (int q = 0; q < nb; ++q)
+    if (panel_parts(q) > 1) panel_slots += nb * panel_parts(q);
+  const int upd_slots = upd_parts > 1 ? NB2 * upd_parts : 0;
+  const int slots_per_col = 2 * panel_slots + 2 * upd_slots;
+  constexpr int kRing = 4;  // columns of partial slots in flight (see the reuse argument below)
   // counter spaces
   const long cAord = 0, cAfin = cAord + T * NB2, cLblk = cAfin + T, cLfin = cLblk + T * NB2,
              cXblk = cLfin + T, cXfin = cXblk + static_cast<long>(N) * NB2, cTblk = cXfin + N,
-             cWfin = cTblk + static_cast<long>(N) * NB2, cEnd = cWfin + T;
+             cWfin = cTblk + static_cast<long>(N) * NB2, cXrow = cWfin + T, cArrive = cXrow + static_cast<long>(N) * nb,
+             cEnd = cArrive + static_cast<long>(N) * slots_per_col;
   P.counters = cEnd;
-  P.scratch_doubles = static_cast<size_t>(N) * bp * bp;
+  const size_t t_doubles = static_cast<size_t>(N) * bp * bp;
+  P.scratch_doubles = t_doubles + static_cast<size_t>(kRing) * slots_per_col * kB * kB;
   P.logdet_doubles = static_cast<size_t>(N) * nb;
   auto aord = [&](long s, int p, int q) { return static_cast<int>(cAord + s * NB2 + p * nb + q); };
   auto afin = [&](long s) { return static_cast<int>(cAfin + s); };
@@ -119,11 +206,13 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
   auto lfin = [&](long s) { return static_cast<int>(cLfin + s); };
   auto xblk = [&](int j, int p, int q) { return static_cast<int>(cXblk + static_cast<long>(j) * NB2 + p * nb + q); };
   auto xfin = [&](int j) { return static_cast<int>(cXfin + j); };
-  auto tblk = [&](int j, int p, int q) { return static_cast<int>(cTblk + static_cast<long>(j) * NB2 + p * nb + q); };
+  auto tcnt = [&](int j, int p, int q) { return static_cast<int>(cTblk + static_cast<long>(j) * NB2 + p * nb + q); };
   auto wfin = [&](long s) { return static_cast<int>(cWfin + s); };
+  auto xrowc = [&](int j, int q) { return static_cast<int>(cXrow + static_cast<long>(j) * nb + q); };
   const int xdone = nb * (nb + 1) / 2;
   const long long tsz = static_cast<long long>(bp) * bp;
 
+  P.slot_tiles = F.tiles();
   Builder B(P);
   std::vector<int> ord(static_cast<size_t>(T), 0);  // update columns applied so far, per tile
 
@@ -149,32 +238,38 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
     const long ds = F.col_start(j);
     const int U = ord[static_cast<size_t>(ds)];
     const int valid = static_cast<int>(std::min<long>(L.b, L.n - static_cast<long>(j) * L.b));
+    std::vector<int> krows;
+    std::vector<long> ks;
+    for (const int* r = F.rows_begin(j); r != F.rows_end(j); ++r)
+      if (*r > j) {
+        krows.push_back(*r);
+        ks.push_back(F.slot(*r, j));
+      }
     // ---- diagonal-tile chain (queue 0): blocked POTRF + TRTRI of tile (j, j)
-    // Fat leaf: factor + invert block (kk, kk), then (kk + 1 < nb) the next
-    // panel block L(kk+1, kk) = A(kk+1, kk) X_kk^T and the next diagonal block
-    // update A(kk+1, kk+1) -= L(kk+1, kk) L(kk+1, kk)^T in the same task, so the
-    // tile's diagonal chain advances one block per task.
+    // Fat leaf: factor + invert block (kk, kk), then (kk + 1 < nb, after the
+    // second-phase dependencies) the next panel block L(kk+1, kk) = A(kk+1, kk)
+    // X_kk^T and the next diagonal block update A(kk+1, kk+1) -= L L^T.
     auto leaf = [&](int kk) {
-      std::vector<Dep> d{{aord(ds, kk, kk), U + kk}};
-      std::vector<int> sg{lblk(ds, kk, kk), lfin(ds), xblk(j, kk, kk), xfin(j)};
+      std::vector<Dep> d{{aord(ds, kk, kk), U + kk}}, d2;
+      std::vector<int> sg{lblk(ds, kk, kk), lfin(ds), xblk(j, kk, kk), xfin(j), xrowc(j, kk)};
       const bool fat = fat_leaf && kk + 1 < nb;
       if (fat) {
-        d.push_back({aord(ds, kk + 1, kk), U + kk});
-        d.push_back({aord(ds, kk + 1, kk + 1), U + kk});
+        d2.push_back({aord(ds, kk + 1, kk), U + kk});
+        d2.push_back({aord(ds, kk + 1, kk + 1), U + kk});
         sg.push_back(lblk(ds, kk + 1, kk));
         sg.push_back(lfin(ds));
         sg.push_back(aord(ds, kk + 1, kk + 1));
       }
-      DTask& t = B.add(0, d, sg);
+      DTask& t = B.add(0, d, sg, d2);
+      t.sig2_count = fat ? 3 : 0;
       t.kind = kLeafTask;
       t.mode = fat ? 2 : 0;
       t.c_off = t.c0_off = t.cm_off = blk_off(ds, bp, kk, kk);
       t.diag_off = static_cast<long long>(j) * nb + kk;
       t.m0 = valid - kk * kB;
       t.n0 = static_cast<int>(static_cast<long>(j) * L.b + kk * kB);
-      t.seg_count = 0;
-      if (kk + 1 < nb) P.zero.push_back(ZeroStrip{blk_off(ds, bp, kk, kk) + kB, nb - 1 - kk, 0});
       t.ldc = t.ldc0 = bp;
+      if (kk + 1 < nb) P.zero.push_back(ZeroStrip{blk_off(ds, bp, kk, kk) + kB, nb - 1 - kk, 0});
       P.task_flops += 2.0 * (kB * kB * kB / 6.0) * 2;  // chol + inverse of the leaf
       if (fat) P.task_flops += 2.0 * kB * kB * kB * 2;
     };
@@ -192,48 +287,136 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
       t.c_off = t.c0_off = blk_off(ds, bp, i, p);
       B.seg(t, kStoreL, blk_off(ds, bp, i, kk), kStoreL, blk_off(ds, bp, p, kk), 0, kB, kTransB | kNegate);
     };
-    auto trow = [&](int kk, int k) {
-      std::vector<Dep> d;
-      for (int l = k; l < kk; ++l) {
-        d.push_back({lblk(ds, kk, l), 1});
-        d.push_back({xblk(j, l, k), 1});
-      }
-      DTask& t = B.add(0, d, {tblk(j, kk, k)});
+    // X_j off-diagonal blocks, assembled right-looking so that row kk of X is
+    // one task behind leaf kk:  T(kk, k) = sum_{l=k}^{kk-1} L(kk, l) X(l, k)
+    // accumulated term by term (tterm, ascending l), X(kk, k) = -X(kk, kk) T(kk, k).
+    auto tterm = [&](int kk, int k, int l) {
+      DTask& t = B.add(0, {{lblk(ds, kk, l), 1}, {xblk(j, l, k), 1}, {tcnt(j, kk, k), l - k}}, {tcnt(j, kk, k)});
       t.kind = kGemmTask;
       t.c_store = kStoreScratch;
       t.c_off = tsz * j + static_cast<long long>(kk) * kB * bp + k * kB;
-      for (int l = k; l < kk; ++l) B.seg(t, kStoreL, blk_off(ds, bp, kk, l), kStoreP1, blk_off(ds, bp, l, k), 0, kB, 0);
+      if (l > k) {
+        t.c0_store = kStoreScratch;
+        t.c0_off = t.c_off;
+      }
+      B.seg(t, kStoreL, blk_off(ds, bp, kk, l), kStoreP1, blk_off(ds, bp, l, k), 0, kB, 0);
     };
     auto xrow = [&](int kk, int k) {
-      DTask& t = B.add(0, {{xblk(j, kk, kk), 1}, {tblk(j, kk, k), 1}}, {xblk(j, kk, k), xfin(j)});
+      DTask& t = B.add(0, {{xblk(j, kk, kk), 1}, {tcnt(j, kk, k), kk - k}}, {xblk(j, kk, k), xfin(j), xrowc(j, kk)});
       t.kind = kGemmTask;
       t.c_store = kStoreP1;
       t.c_off = blk_off(ds, bp, kk, k);
       B.seg(t, kStoreP1, blk_off(ds, bp, kk, kk), kStoreScratch,
             tsz * j + static_cast<long long>(kk) * kB * bp + k * kB, 0, kB, kNegate);
     };
+    // ---- critical tail, progressive with the chain: the panels of the first
+    // two off-diagonal tiles L(k, j) = A(k, j) X_j^T by block column q as soon
+    // as row q of X_j is complete (split-K over parts of <= 128 when K > 256),
+    // and the updates of tiles (k0, k0) -- the next diagonal tile when k0 = j+1
+    // -- and (k1, k0) -- the next column's first panel tile -- split over
+    // k-block pairs, each part issued once its panel columns exist.  The
+    // reducer of an update waits (second phase) for the block's earlier updates.
+    auto panel_prog = [&](size_t ia, int q, int queue, int slot_base) {
+      const long sk = ks[ia];
+      const int Uk = ord[static_cast<size_t>(sk)];
+      const int parts = panel_parts(q), K = (q + 1) * kB;
+      int base = slot_base;
+      for (int qq = 0; qq < q; ++qq) base += panel_parts(qq) > 1 ? nb * panel_parts(qq) : 0;
+      for (int p = 0; p < nb; ++p) {
+        for (int r = 0; r < parts; ++r) {
+          DTask& t = B.add(queue, {{afin(sk), Uk * NB2}, {xrowc(j, q), q + 1}}, {lblk(sk, p, q), lfin(sk)});
+          t.kind = parts > 1 ? kSplitTask : kGemmTask;
+          t.c_store = kStoreL;
+          t.c_off = blk_off(sk, bp, p, q);
+          t.m0 = p * kB;
+          t.n0 = q * kB;
+          if (parts > 1) {
+            const int slot = base + p * parts;
+            t.p_off = static_cast<long long>(t_doubles) +
+                      (static_cast<long long>(j % kRing) * slots_per_col + slot) * kB * kB;
+            t.aux0 = static_cast<int>(cArrive + static_cast<long>(j) * slots_per_col + slot);
+            t.aux1 = (r << 8) | parts;
+          }
+          const int klo = parts > 1 ? r * 2 * kB : 0, khi = parts > 1 ? std::min(K, (r + 1) * 2 * kB) : K;
+          B.seg(t, kStoreA, tile_off(sk, bp), kStoreP1, tile_off(ds, bp), klo, khi, kTransB);
+        }
+      }
+    };
+    // k-blocks [2r, 2r + 2) of the update of tile (krows[ia], krows[ic]); u = its ordinal
+    auto update_split = [&](size_t ia, size_t ic, int r, int u, int queue, int slot_base) {
+      const int a = krows[ia], c = krows[ic];
+      const long ts = F.slot(a, c);
+      if (ts < 0) throw Error(kErrConsistency, "update target outside the filled pattern");
+      const int klo = upd_parts > 1 ? 2 * r : 0, khi = upd_parts > 1 ? std::min(nb, 2 * r + 2) : nb;
+      for (int p = 0; p < nb; ++p)
+        for (int q = 0; q < (a == c ? p + 1 : nb); ++q) {
+          std::vector<Dep> d;
+          for (int k = klo; k < khi; ++k) {
+            d.push_back({lblk(ks[ia], p, k), 1});
+            if (!(ia == ic && q == p)) d.push_back({lblk(ks[ic], q, k), 1});
+          }
+          std::vector<Dep> d2{{aord(ts, p, q), u}};
+          if (upd_parts == 1) d.insert(d.end(), d2.begin(), d2.end());
+          std::vector<int> sg{aord(ts, p, q)};
+          if (a != c) sg.push_back(afin(ts));
+          DTask& t = B.add(queue, d, sg, upd_parts > 1 ? d2 : std::vector<Dep>{});
+          t.kind = upd_parts > 1 ? kSplitTask : kGemmTask;
+          t.c_store = t.c0_store = kStoreA;
+          t.c_off = t.c0_off = blk_off(ts, bp, p, q);
+          t.m0 = p * kB;
+          t.n0 = q * kB;
+          if (upd_parts > 1) {
+            // the parts of one block are emitted in different steps of the chain,
+            // so their slots are addressed by block index
+            const int slot = slot_base + (p * nb + q) * upd_parts;
+            t.p_off = static_cast<long long>(t_doubles) +
+                      (static_cast<long long>(j % kRing) * slots_per_col + slot) * kB * kB;
+            t.aux0 = static_cast<int>(cArrive + static_cast<long>(j) * slots_per_col + slot);
+            t.aux1 = (r << 8) | upd_parts;
+          }
+          B.seg(t, kStoreL, tile_off(ks[ia], bp), kStoreL, tile_off(ks[ic], bp), klo * kB, khi * kB,
+                kTransB | kNegate);
+        }
+    };
+    const bool tail0 = !krows.empty(), tail1 = krows.size() > 1;
+    int u00 = 0, u10 = 0;
+    if (tail0) u00 = ord[static_cast<size_t>(F.slot(krows[0], krows[0]))]++;
+    if (tail1) u10 = ord[static_cast<size_t>(F.slot(krows[1], krows[0]))]++;
+    const int upd_step_parts = upd_parts;  // parts issued at chain steps kk = 1, 3, 5, ... and nb - 1
+    auto upd_part_at = [&](int kk) {
+      if (upd_step_parts > 1) return (kk % 2 == 1 || kk == nb - 1) ? kk / 2 : -1;
+      return kk == nb - 1 ? 0 : -1;
+    };
+
     for (int kk = 0; kk < nb; ++kk) {
       leaf(kk);
-      if (!fat_leaf && kk + 1 < nb) {
+      if (kk + 1 < nb && !fat_leaf) {
         paneld(kk + 1, kk);
         traild(kk + 1, kk + 1, kk);
       }
       for (int k = 0; k < kk; ++k) xrow(kk, k);
+      for (int k = 0; k <= kk && kk + 1 < nb; ++k) tterm(kk + 1, k, kk);
       for (int i = kk + 2; i < nb; ++i) paneld(i, kk);
       for (int p = kk + 1; p < nb; ++p)
         for (int i = p; i < nb; ++i)
           if (!(i == kk + 1 && p == kk + 1)) traild(i, p, kk);
-      if (kk + 1 < nb)
-        for (int k = 0; k <= kk; ++k) trow(kk + 1, k);
-    }
-    // ---- bulk (queue 1)
-    std::vector<int> krows;
-    std::vector<long> ks;
-    for (const int* r = F.rows_begin(j); r != F.rows_end(j); ++r)
-      if (*r > j) {
-        krows.push_back(*r);
-        ks.push_back(F.slot(*r, j));
+      for (int kk2 = kk + 2; kk2 < nb; ++kk2)
+        for (int k = 0; k <= kk; ++k) tterm(kk2, k, kk);
+      if (tail0) {
+        panel_prog(0, kk, 0, 0);
+        const int r = upd_part_at(kk);
+        if (r >= 0) update_split(0, 0, r, u00, 0, 2 * panel_slots);
       }
+    }
+    if (tail1) {
+      // second tile: same progression, issued on the bulk queue right after the chain
+      for (int kk = 0; kk < nb; ++kk) {
+        panel_prog(1, kk, 1, panel_slots);
+        const int r = upd_part_at(kk);
+        if (r >= 0) update_split(1, 0, r, u10, 1, 2 * panel_slots + upd_slots);
+      }
+    }
+    // ---- bulk (queue 1): the other panels, the other updates, deferred W
     auto panel = [&](size_t ia) {
       const long sk = ks[ia];
       const int Uk = ord[static_cast<size_t>(sk)];
@@ -266,20 +449,14 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
           B.seg(t, kStoreL, tile_off(ks[ia], bp), kStoreL, tile_off(ks[ic], bp), 0, bp, kTransB | kNegate);
         }
     };
-    if (!krows.empty()) {
-      panel(0);
-      update(0, 0);  // feeds the next diagonal tile
-      for (size_t ia = 1; ia < krows.size(); ++ia) panel(ia);
-      for (size_t ia = 1; ia < krows.size(); ++ia) update(ia, 0);
-      for (size_t ic = 1; ic < krows.size(); ++ic)
-        for (size_t ia = ic; ia < krows.size(); ++ia) update(ia, ic);
-    }
+    for (size_t ia = 2; ia < krows.size(); ++ia) panel(ia);
+    for (size_t ia = 2; ia < krows.size(); ++ia) update(ia, 0);
+    for (size_t ic = 1; ic < krows.size(); ++ic)
+      for (size_t ia = ic; ia < krows.size(); ++ia) update(ia, ic);
     if (j - defer_w >= 0) emit_w(j - defer_w);
   }
   for (int j = std::max(0, N - defer_w); j < N; ++j) emit_w(j);
-  const std::vector<int> pos = B.finish(crit_workers);
-  std::vector<int> order(pos.begin(), pos.end());
-  validate_dataflow(P, order);
+  B.finish(crit_workers, chain);
   return P;
 }
 
@@ -303,6 +480,7 @@ DataflowPlan build_phase2_dataflow(const Pattern& F, const Closure& sel, int cri
     return s;
   };
   auto final_count = [&](long s) { return C.tiles()[static_cast<size_t>(s)].i == C.tiles()[static_cast<size_t>(s)].j ? nb * (nb + 1) / 2 : NB2; };
+  P.slot_tiles = C.tiles();
   Builder B(P);
   for (const ColumnWork& cw : sel.columns) {
     const int i = cw.col;
@@ -434,9 +612,7 @@ DataflowPlan build_phase2_dataflow(const Pattern& F, const Closure& sel, int cri
         if (o.has_crit && o.j == kcrit) emit_crit(o, 0);
     }
   }
-  const std::vector<int> pos = B.finish(crit_workers);
-  std::vector<int> order(pos.begin(), pos.end());
-  validate_dataflow(P, order);
+  B.finish(crit_workers);
   return P;
 }
 

@@ -30,6 +30,15 @@ struct DataflowPlan {
   // phase-1 stores (upper triangle of the diagonal tiles): origin offset and
   // width in 64-column blocks; cleared by a separate kernel before the sweep.
   std::vector<ZeroStrip> zero;
+  std::vector<Coord> slot_tiles;  // tile coordinates of the store slots (diagnostics: task traces)
+  // push-model scheduling tables (finalize_waiters): per task the number of
+  // first-phase dependencies not satisfied initially, per counter its waiters
+  // (CSR, sorted by value), and the initially ready tasks of each queue
+  // waiters of counter c reaching value v: wl[vidx[vbase[c] + v] .. vidx[vbase[c] + v + 1]),
+  // for 1 <= v <= vbase[c + 1] - vbase[c] - 2
+  std::vector<int> need, vbase, vidx, init0, init1;
+  std::vector<int> wl;
+  std::vector<DTask> chain;  // leaf steps of the chain task (kChainTask), in order
 };
 
 // Fused factorization + phase 1 over the FILLED pattern: per column, the
@@ -37,7 +46,9 @@ struct DataflowPlan {
 // rows) on queue 0; panel GEMMs L_kj = A_kj X_j^T, Schur updates (critical
 // column first) and deferred W_kj = L_kj X_j on queue 1.
 // fat_leaf fuses the next panel block and diagonal-block update into the leaf task.
-DataflowPlan build_factor_dataflow(const Pattern& filled, int crit_workers, int defer_w, bool fat_leaf);
+// chain: the leaves (fat) become the steps of one persistent chain task per matrix.
+DataflowPlan build_factor_dataflow(const Pattern& filled, int crit_workers, int defer_w, bool fat_leaf,
+                                   bool chain = false);
 
 // Phase 2 over a closure: per column descending, off-diagonal targets split
 // into an early part and the k == j term, diagonal targets into LAUUM + early

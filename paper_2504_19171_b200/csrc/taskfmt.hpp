@@ -56,23 +56,38 @@ struct Task {
   unsigned char diag_store, pad0, pad1, pad2;
 };
 
-enum TaskKind : unsigned char { kGemmTask = 0, kLeafTask = 1 };
+enum TaskKind : unsigned char { kGemmTask = 0, kLeafTask = 1, kSplitTask = 2, kChainTask = 3 };
 
 // One schedulable unit of a sweep.  kGemmTask: C / C0 / Cm / diag stores and
 // offsets as Task, segments [seg_begin, seg_begin + seg_count).  kLeafTask:
 // c_off = A block (input, ld = ldc0), c0_off = L block, cm_off = X block
 // (ld = ldc), diag_off = logdet slot, m0 = valid rows, n0 = global pivot
-// index of the block's first row, mode = 0 factor + invert / 1 invert only,
-// seg_count = number of 64-column blocks right of the diagonal block to zero
-// in the L and X rows.
+// index of the block's first row, mode = 0 factor + invert / 1 invert only
+// (| 2: fat leaf, also the next panel block and next diagonal-block update).
+// kSplitTask: one K-part of a split-K block GEMM: writes its partial product
+// to scratch slot p_off + part * 64*64, bumps the arrival counter aux0, and
+// the last of the `parts` arrivals (aux1 = part << 8 | parts) reduces all
+// partials in part order (deterministic), adds C0 and runs the epilogue of
+// `mode` like a kGemmTask.  Only the reducer signals.
+// kChainTask: the whole diagonal chain of one matrix run by one CTA: steps
+// [seg_begin, seg_begin + seg_count) of the plan's chain list, each a (fat)
+// leaf descriptor executed in order, waiting on its own dependencies and
+// keeping the next diagonal block in shared memory between steps.
+// Dependencies: deps [dep_begin, dep_begin + dep_count) are waited before the
+// task starts; the next dep2_count are waited before its second phase (the
+// fat part of a leaf, the reduction of a split task) -- typically the
+// update-ordering counter of the block it writes.  Signals: the last
+// sig2_count of a leaf's signals are raised after its second phase, the
+// others as soon as its first phase is done.
 struct DTask {
-  long long c_off, c0_off, cm_off, diag_off;
+  long long c_off, c0_off, cm_off, diag_off, p_off;
   int ldc, ldc0;
   int m0, n0;
   int seg_begin, seg_count;
   int dep_begin, sig_begin;
+  int aux0, aux1;
   unsigned short dep_count, sig_count;
-  unsigned char kind, mode, c_store, c0_store, cm_store, diag_store, pad0, pad1;
+  unsigned char kind, mode, c_store, c0_store, cm_store, diag_store, dep2_count, sig2_count;
 };
 
 // wait until counters[counter] >= value
@@ -88,9 +103,14 @@ struct ZeroStrip {
 };
 
 // A queue is a contiguous range of the task array; `workers` CTAs serve q0
-// (the critical chain), the rest of the grid serves q1.
+// (the critical chain) only, the rest of the grid serves q0 first, then q1.
 struct QueueDesc {
   int first, count, workers, pad;
 };
+
+// Push-model scheduling (plan.hpp vbase / vidx / wl): for every counter and
+// value, the tasks whose dependency that value completes.  The task whose
+// signal brings a counter to the value decrements each such waiter's
+// missing-dependency count, and the one that reaches zero enqueues it.
 
 }  // namespace tib

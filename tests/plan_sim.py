@@ -31,10 +31,28 @@ class Sim:
         self.status = status  # list with first bad pivot
 
     def ready(self, t):
-        d = self.p["deps"][t["dep_begin"]:t["dep_begin"] + t["dep_count"]]
+        d = self.p["deps"][t["dep_begin"]:t["dep_begin"] + t["dep_count"] + t["dep2_count"]]
         return all(self.cnt[c] >= v for c, v in zip(d["counter"], d["value"]))
 
     def gemm(self, t):
+        """Block GEMM task; a split task (kind 2) stores its partial and only
+        the last of its group reduces (in part order) and signals."""
+        acc = self.product(t)
+        if t["kind"] == 2:
+            part, parts = int(t["aux1"]) >> 8, int(t["aux1"]) & 255
+            slots = self.s[K_STORE["SCRATCH"]]
+            base = int(t["p_off"])
+            slots[base + part * BLK * BLK: base + (part + 1) * BLK * BLK] = acc.reshape(-1)
+            self.cnt[int(t["aux0"])] += 1
+            if self.cnt[int(t["aux0"])] < parts:
+                return False
+            acc = slots[base: base + parts * BLK * BLK].reshape(parts, BLK, BLK)[0].copy()
+            for q in range(1, parts):
+                acc = acc + slots[base + q * BLK * BLK: base + (q + 1) * BLK * BLK].reshape(BLK, BLK)
+        self.epilogue(t, acc)
+        return True
+
+    def product(self, t):
         acc = np.zeros((BLK, BLK))
         for g in self.p["segs"][t["seg_begin"]:t["seg_begin"] + t["seg_count"]]:
             klo, khi = int(g["k_lo"]), int(g["k_hi"])
@@ -52,6 +70,9 @@ class Sim:
                 opb = view(B, int(g["b_off"]) + klo * ldb + n0, khi - klo, BLK, ldb)
             prod = opa @ opb
             acc += -prod if g["flags"] & NEGATE else prod
+        return acc
+
+    def epilogue(self, t, acc):
         ldc = int(t["ldc"])
         if t["c0_store"] != NONE:
             acc = acc + view(self.s[int(t["c0_store"])], int(t["c0_off"]), BLK, BLK, int(t["ldc0"]))
@@ -108,7 +129,10 @@ class Sim:
                     break
             else:
                 raise RuntimeError(f"dataflow deadlock: heads {head}")
-            (self.leaf if t["kind"] == 1 else self.gemm)(t)
+            if t["kind"] == 1:
+                self.leaf(t)
+            elif not self.gemm(t):
+                continue
             sg = self.p["sigs"][t["sig_begin"]:t["sig_begin"] + t["sig_count"]]
             np.add.at(self.cnt, sg, 1)
 

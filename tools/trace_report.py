@@ -9,12 +9,12 @@ import sys
 import numpy as np
 
 DTASK = np.dtype({
-    "names": ["c_off", "c0_off", "cm_off", "diag_off", "ldc", "ldc0", "m0", "n0", "seg_begin", "seg_count",
-              "dep_begin", "sig_begin", "dep_count", "sig_count", "kind", "mode", "c_store", "c0_store",
-              "cm_store", "diag_store"],
-    "formats": ["<i8"] * 4 + ["<i4"] * 8 + ["<u2"] * 2 + ["u1"] * 6,
-    "offsets": [0, 8, 16, 24, 32, 36, 40, 44, 48, 52, 56, 60, 64, 66, 68, 69, 70, 71, 72, 73],
-    "itemsize": 80,
+    "names": ["c_off", "c0_off", "cm_off", "diag_off", "p_off", "ldc", "ldc0", "m0", "n0", "seg_begin", "seg_count",
+              "dep_begin", "sig_begin", "aux0", "aux1", "dep_count", "sig_count", "kind", "mode", "c_store",
+              "c0_store", "cm_store", "diag_store", "dep2_count"],
+    "formats": ["<i8"] * 5 + ["<i4"] * 10 + ["<u2"] * 2 + ["u1"] * 7,
+    "offsets": [0, 8, 16, 24, 32, 40, 44, 48, 52, 56, 60, 64, 68, 72, 76, 80, 82, 84, 85, 86, 87, 88, 89, 90],
+    "itemsize": 96,
 })
 DEP = np.dtype([("counter", "<i4"), ("value", "<i4")])
 SEG = np.dtype({
@@ -28,21 +28,40 @@ STORE = {0: "A", 1: "L", 2: "P1", 3: "S", 5: "T", 255: "-"}
 
 def load(path):
     with open(path, "rb") as f:
-        hdr = np.frombuffer(f.read(64), np.int64)
-        if hdr[0] != -2:
+        hdr = np.frombuffer(f.read(80), np.int64)
+        if hdr[0] != -3:
             raise SystemExit(f"{path}: old trace format")
-        ntask, batch, nq0, nb, ndep, nsig, nseg = (int(x) for x in hdr[1:])
-        tasks = np.frombuffer(f.read(80 * ntask), DTASK)
+        ntask, batch, nq0, nb, ndep, nsig, nseg, ntiles, bp = (int(x) for x in hdr[1:])
+        tasks = np.frombuffer(f.read(DTASK.itemsize * ntask), DTASK)
         deps = np.frombuffer(f.read(8 * ndep), DEP)
         sigs = np.frombuffer(f.read(4 * nsig), np.int32)
         segs = np.frombuffer(f.read(32 * nseg), SEG)
+        tiles = np.frombuffer(f.read(8 * ntiles), np.int32).reshape(-1, 2)
         rec = np.frombuffer(f.read(), np.uint64).reshape(-1, 4)
-    return dict(ntask=ntask, batch=batch, nq0=nq0, nb=nb, tasks=tasks, deps=deps, sigs=sigs, segs=segs, rec=rec)
+    return dict(ntask=ntask, batch=batch, nq0=nq0, nb=nb, tasks=tasks, deps=deps, sigs=sigs, segs=segs, rec=rec,
+                tiles=tiles, bp=bp)
+
+
+def where(t, tiles, bp):
+    """(tile i, tile j, block p, block q) of a task's output block, or the leaf's block."""
+    off = int(t["c0_off"] if t["kind"] == 1 else t["c_off"])
+    if t["c_store"] in (5,) and t["kind"] != 1:  # scratch: T blocks, per column j
+        j, rem = divmod(off, bp * bp)
+        return ("T", j, rem // bp // 64, rem % bp // 64)
+    slot, rem = divmod(off, bp * bp)
+    if slot >= len(tiles):
+        return ("?", slot, 0, 0)
+    i, j = tiles[slot]
+    return (int(i), int(j), rem // bp // 64, rem % bp // 64)
 
 
 def label(t, q0):
     if t["kind"] == 1:
         return "leaf" + ("+fat" if t["mode"] & 2 else "")
+    if t["kind"] == 2:
+        sp = f"/split{int(t['aux1']) & 255}"
+    else:
+        sp = ""
     cs, c0 = STORE.get(int(t["c_store"]), "?"), STORE.get(int(t["c0_store"]), "?")
     q = "q0" if q0 else "q1"
     name = {("q0", "L"): "paneld", ("q0", "A"): "traild", ("q0", "T"): "trow", ("q0", "P1"): "xrow",
@@ -52,7 +71,7 @@ def label(t, q0):
             name = {0: "off", 1: "symdiag", 2: "mirror"}[int(t["mode"])] + ("+c0" if c0 == "S" else "")
         else:
             name = f"{cs}"
-    return f"{q}:{name}/s{int(t['seg_count'])}"
+    return f"{q}:{name}/s{int(t['seg_count'])}{sp}"
 
 
 def report(path):
@@ -60,12 +79,15 @@ def report(path):
     tasks, deps, sigs, rec, batch, nq0 = d["tasks"], d["deps"], d["sigs"], d["rec"], d["batch"], d["nq0"]
     ok = rec[:, 2] > 0
     rec = rec[ok]
-    claim, ready, done = (rec[:, i].astype(np.float64) / 1e3 for i in range(3))  # us
+    claim, pushed, done = (rec[:, i].astype(np.float64) / 1e3 for i in range(3))  # us
+    # v3 traces: field 1 = time the task was pushed to a ready queue (0: ready at start)
+    ready = claim.copy()
     tidx = (rec[:, 3] >> 32).astype(np.int64)
     mat = ((rec[:, 3] >> 16) & 0xFFFF).astype(np.int64)
     sm = (rec[:, 3] & 0xFFFF).astype(np.int64)
     t0 = claim.min()
-    claim, ready, done = claim - t0, ready - t0, done - t0
+    pushed = np.where(pushed > 0, pushed, claim.min() * 1e0)
+    claim, ready, done, pushed = claim - t0, ready - t0, done - t0, pushed - t0
     span = done.max()
     q0 = tidx < nq0
     labels = np.array([label(tasks[i], i < nq0) for i in range(len(tasks))])
@@ -96,8 +118,18 @@ def report(path):
     # ---- critical path
     key = {(int(t), int(mm)): r for r, (t, mm) in enumerate(zip(tidx, mat))}
     events = collections.defaultdict(list)  # (counter, mat) -> [(done, rec)]
+    # split groups signal once, through the reducer (the part that finished last)
+    reducer = {}
     for r in range(len(rec)):
         t = tasks[tidx[r]]
+        if t["kind"] == 2:
+            g = (int(t["aux0"]), int(mat[r]))
+            if g not in reducer or done[r] > done[reducer[g]]:
+                reducer[g] = r
+    for r in range(len(rec)):
+        t = tasks[tidx[r]]
+        if t["kind"] == 2 and reducer[(int(t["aux0"]), int(mat[r]))] != r:
+            continue
         for s in range(t["sig_begin"], t["sig_begin"] + t["sig_count"]):
             events[(int(sigs[s]), int(mat[r]))].append((done[r], r))
     for v in events.values():
@@ -106,7 +138,15 @@ def report(path):
     for r in np.argsort(done):
         by_sm[int(sm[r])].append(r)
     sm_done = {s: np.array([done[r] for r in rs]) for s, rs in by_sm.items()}
+    # queue wait: claim time minus the time the task was pushed ready
+    qwait = claim - pushed
+    for name, m in (("q0", q0), ("q1", ~q0)):
+        w = qwait[m]
+        if len(w):
+            print(f"  {name} queue wait (claim - pushed): mean {w.mean():.2f} us, p50 {np.median(w):.2f}, p90 "
+                  f"{np.percentile(w, 90):.2f}, max {w.max():.1f}")
     r = int(np.argmax(done))
+    path_seq = []
     path_exec = collections.Counter()
     path_n = collections.Counter()
     gap_dep = gap_claim = 0.0
@@ -114,10 +154,11 @@ def report(path):
     while r is not None and steps < 10 ** 7:
         steps += 1
         t = tasks[tidx[r]]
+        path_seq.append(r)
         path_exec[lab[r]] += done[r] - ready[r]
         path_n[lab[r]] += 1
         best, bt = None, -1.0
-        for k in range(t["dep_begin"], t["dep_begin"] + t["dep_count"]):
+        for k in range(t["dep_begin"], t["dep_begin"] + t["dep_count"] + t["dep2_count"]):
             dp = deps[k]
             ev = events.get((int(dp["counter"]), int(mat[r])), [])
             if dp["value"] <= 0 or len(ev) < dp["value"]:
@@ -125,26 +166,28 @@ def report(path):
             tm, pr = ev[dp["value"] - 1]
             if tm > bt:
                 best, bt = pr, tm
-        if best is not None and bt >= claim[r] - 0.5:
-            gap_dep += max(0.0, ready[r] - bt)
-            r = best
-            continue
-        # claimed late: follow the task that freed a CTA on this SM
-        gap_dep += max(0.0, ready[r] - max(bt, claim[r]))
-        arr = sm_done[int(sm[r])]
-        i = np.searchsorted(arr, claim[r] + 1e-3) - 1
-        if i < 0:
+        if best is None:
             break
-        prev = by_sm[int(sm[r])][i]
-        gap_claim += max(0.0, claim[r] - done[prev])
-        path_exec["(claim-wait)"] += 0
-        r = prev if prev != r else None
+        # queue wait before the claim (or second-phase wait inside the task)
+        gap_claim += max(0.0, claim[r] - bt)
+        r = best
     tot = sum(path_exec.values())
-    print(f"  critical path: {sum(path_n.values())} tasks, exec {tot / 1e3:.1f} ms, dep-latency {gap_dep / 1e3:.1f} ms, "
-          f"claim gaps {gap_claim / 1e3:.1f} ms (span {span / 1e3:.1f} ms)")
+    print(f"  critical path: {sum(path_n.values())} tasks, exec {tot / 1e3:.1f} ms, "
+          f"queue waits {gap_claim / 1e3:.1f} ms (span {span / 1e3:.1f} ms)")
     for L, v in path_exec.most_common():
         if path_n[L]:
             print(f"    {L:28s} n={path_n[L]:6d} exec {v / 1e3:8.2f} ms  mean {v / path_n[L]:6.1f} us")
+    # a window of the path from the middle of the sweep, in time order
+    seq = path_seq[::-1]
+    mid = len(seq) // 2
+    print("  critical path sample (claim, ready, done us; class; tile i, j; block p, q):")
+    prev_done = None
+    for r in seq[mid:mid + 60]:
+        t = tasks[tidx[r]]
+        w = where(t, d["tiles"], d["bp"])
+        gap = "" if prev_done is None else f" (+{ready[r] - prev_done:.1f})"
+        print(f"    {claim[r]:10.1f} {ready[r]:10.1f} {done[r]:10.1f}{gap:>9s}  {lab[r]:26s} {w}")
+        prev_done = done[r]
 
 
 if __name__ == "__main__":
