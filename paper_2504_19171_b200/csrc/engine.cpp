@@ -243,7 +243,7 @@ static int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e && *e ? std::atoi(e) : dflt;
 }
-static int crit_workers() { return env_int("TIB_CRIT_WORKERS", 4); }
+static int crit_workers() { return env_int("TIB_CRIT_WORKERS", 12); }
 
 static std::shared_ptr<DevPlan> upload_plan(DataflowPlan&& host, int device, cudaStream_t s) {
   auto d = std::make_shared<DevPlan>();
@@ -338,7 +338,7 @@ static const char* trace_prefix() {
 static std::atomic<int> g_trace_seq{0};
 
 static void write_trace(DevPlan& P, int batch, unsigned long long* d_trace, cudaStream_t s) {
-  const size_t n = static_cast<size_t>(P.host.tasks.size()) * batch * 4;
+  const size_t n = (P.host.tasks.size() + P.host.chain.size()) * batch * 4;
   std::vector<unsigned long long> h(n);
   CK(cudaMemcpyAsync(h.data(), d_trace, n * 8, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
@@ -347,7 +347,7 @@ static void write_trace(DevPlan& P, int batch, unsigned long long* d_trace, cuda
   if (!f) return;
   // v2: header, then the raw plan (tasks, deps, sigs, segs) so tools/trace_report.py
   // can rebuild every dependency edge and walk the critical path
-  const long long hdr[10] = {-3,
+  const long long hdr[11] = {-4,
                             static_cast<long long>(P.host.tasks.size()),
                             batch,
                             P.host.q0.count,
@@ -356,7 +356,8 @@ static void write_trace(DevPlan& P, int batch, unsigned long long* d_trace, cuda
                             static_cast<long long>(P.host.sigs.size()),
                             static_cast<long long>(P.host.segs.size()),
                             static_cast<long long>(P.host.slot_tiles.size()),
-                            P.host.bp};
+                            P.host.bp,
+                            static_cast<long long>(P.host.chain.size())};
   std::fwrite(hdr, sizeof(hdr), 1, f);
   std::fwrite(P.host.tasks.data(), sizeof(DTask), P.host.tasks.size(), f);
   std::fwrite(P.host.deps.data(), sizeof(Dep), P.host.deps.size(), f);
@@ -405,7 +406,7 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
   };
   if (trace_prefix()) {
     unsigned long long* d_trace = nullptr;
-    const size_t n = nt * batch * 4;
+    const size_t n = (nt + P.host.chain.size()) * batch * 4;
     CK(cudaMallocAsync(reinterpret_cast<void**>(&d_trace), n * 8, s));
     CK(cudaMemsetAsync(d_trace, 0, n * 8, s));
     a.trace = d_trace;
@@ -497,6 +498,7 @@ static void upload_matrix(const MatrixObj& m, const Pattern& filled, int bp, dou
 
 struct SweepStores {
   DevBuf A, L, P1, scratch, logdet, counters;
+  size_t scratch_stride = 0;  // doubles of scratch per matrix
   DevBuf status;  // DevStatus per matrix (as doubles storage)
   long cstride = 0;  // ints of counters per matrix
   double* ctr(int k) const { return reinterpret_cast<double*>(reinterpret_cast<int*>(counters.p) + cstride * k); }
@@ -507,13 +509,14 @@ static DevBuf alloc_counters(long per_matrix, int batch, int dev, cudaStream_t s
 }
 
 static void alloc_factor_stores(SweepStores& st, const FactorPlan2& P, int batch, int dev, cudaStream_t s,
-                                long min_counters = 0) {
+                                long min_counters = 0, size_t min_scratch = 0) {
   const size_t tile = static_cast<size_t>(P.bp) * P.bp;
   const size_t T = P.sym.filled.size();
   st.A = DevBuf(T * tile * batch, dev, s);
   st.L = DevBuf(T * tile * batch, dev, s);
   st.P1 = DevBuf(T * tile * batch, dev, s);
-  st.scratch = DevBuf(P.flow->host.scratch_doubles * batch, dev, s);
+  st.scratch_stride = std::max(P.flow->host.scratch_doubles, min_scratch);
+  st.scratch = DevBuf(st.scratch_stride * batch, dev, s);
   st.logdet = DevBuf(P.flow->host.logdet_doubles * batch, dev, s);
   st.cstride = std::max<long>(P.flow->host.counters, min_counters);
   st.counters = alloc_counters(st.cstride, batch, dev, s);
@@ -587,7 +590,7 @@ static SigmaObj* selected_inverse_matrix(const MatrixObj& m, const Request& req,
   const Closure sel = symbolic_inversion(select_tiles(F.layout(), F, req), F);
   auto p2 = phase2_plan_for(F, sel, device, s);
   SweepStores st;
-  alloc_factor_stores(st, *fp, 1, device, s, p2->flow->host.counters);
+  alloc_factor_stores(st, *fp, 1, device, s, p2->flow->host.counters, p2->flow->host.scratch_doubles);
   upload_matrix(m, F, fp->bp, st.A.p, s);
   auto* res = new SigmaObj;
   std::unique_ptr<SigmaObj> guard(res);
@@ -910,7 +913,8 @@ int tib_selected_inverse_of_factor(tib_factor f, int preset, const long* rows, c
     res->S = DevBuf(p2->sel.closure.size() * tile, f->device, s);
     res->var = DevBuf(static_cast<size_t>(f->layout.N) * p2->bp, f->device, s);
     DevBuf ctr = alloc_counters(p2->flow->host.counters, 1, f->device, s);
-    std::vector<BaseTable> tables{make_table(nullptr, f->L.p, f->P1.p, res->S.p, res->var.p, nullptr, nullptr, nullptr, ctr.p)};
+    DevBuf scratch(p2->flow->host.scratch_doubles, f->device, s);
+    std::vector<BaseTable> tables{make_table(nullptr, f->L.p, f->P1.p, res->S.p, res->var.p, scratch.p, nullptr, nullptr, ctr.p)};
     phase2_sweep(*p2, s, tables);
     CK(cudaStreamSynchronize(s));
     *out = guard.release();
@@ -1006,7 +1010,7 @@ int tib_selected_inverse_batch(const tib_matrix* ms, int count, int device, doub
     auto p2 = phase2_plan_for(F, sel, device, s);
     const size_t tile = static_cast<size_t>(fp->bp) * fp->bp;
     SweepStores st;
-    alloc_factor_stores(st, *fp, count, device, s, p2->flow->host.counters);
+    alloc_factor_stores(st, *fp, count, device, s, p2->flow->host.counters, p2->flow->host.scratch_doubles);
     DevBuf Sg(p2->sel.closure.size() * tile * count, device, s);
     DevBuf var(static_cast<size_t>(m0.layout.N) * fp->bp * count, device, s);
     std::vector<BaseTable> tables;
@@ -1015,7 +1019,7 @@ int tib_selected_inverse_batch(const tib_matrix* ms, int count, int device, doub
       upload_matrix(*ms[k], F, fp->bp, st.A.p + T * tile * k, s);
       tables.push_back(make_table(st.A.p + T * tile * k, st.L.p + T * tile * k, st.P1.p + T * tile * k,
                                   Sg.p + p2->sel.closure.size() * tile * k, var.p + static_cast<size_t>(m0.layout.N) * fp->bp * k,
-                                  st.scratch.p + fp->flow->host.scratch_doubles * k,
+                                  st.scratch.p + st.scratch_stride * k,
                                   st.logdet.p + fp->flow->host.logdet_doubles * k, st.status.p + k, st.ctr(k)));
     }
     factor_sweep(*fp, st, s, tables);
@@ -1103,7 +1107,7 @@ int tib_resident_create(tib_matrix m, int device, tib_resident* out) {
     const Flops fl = count_flops(r->fp->sym, &r->p2->sel);
     r->model_flops = fl.total();
     const size_t tile = static_cast<size_t>(r->fp->bp) * r->fp->bp;
-    alloc_factor_stores(r->st, *r->fp, 1, device, s, r->p2->flow->host.counters);
+    alloc_factor_stores(r->st, *r->fp, 1, device, s, r->p2->flow->host.counters, r->p2->flow->host.scratch_doubles);
     r->A0 = DevBuf(F.size() * tile, device, s);
     upload_matrix(*m, F, r->fp->bp, r->A0.p, s);
     r->Sg = DevBuf(r->p2->sel.closure.size() * tile, device, s);

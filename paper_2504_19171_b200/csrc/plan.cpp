@@ -468,8 +468,35 @@ DataflowPlan build_phase2_dataflow(const Pattern& F, const Closure& sel, int cri
   P.nb = nb;
   const Pattern& C = sel.closure;
   const long Tc = static_cast<long>(C.size());
-  const long cSpart = 0, cSfin = cSpart + Tc * NB2;
-  P.counters = cSfin + Tc;
+  const int N = P.L.N;
+  // Split-K partial slots: per column, the parts of its late (critical) targets,
+  // on a ring of kRing columns.  A column's split parts additionally wait for
+  // the targets of the column kRing places later in processing order, which
+  // frees the ring slot (implied by the data dependencies on band patterns,
+  // enforced for any other closure).
+  constexpr int kRing = 4;
+  std::vector<int> col_slots(static_cast<size_t>(N), 0);
+  std::vector<std::vector<int>> Kof(static_cast<size_t>(N));
+  for (const ColumnWork& cw : sel.columns) {
+    const int i = cw.col;
+    std::vector<int>& K = Kof[static_cast<size_t>(i)];
+    for (const int* r = F.rows_begin(i); r != F.rows_end(i); ++r)
+      if (*r > i) K.push_back(*r);
+    if (K.empty()) continue;
+    const int kc = K[0];
+    int n = 0;
+    for (int j : cw.offdiag_rows) {
+      int late = 0;
+      for (int k : K) late += std::min(j, k) == kc ? 1 : 0;
+      if (late > 1) n += NB2 * late;
+    }
+    if (cw.diagonal) n += nb * (nb + 1) / 2 * (1 + static_cast<int>(K.size()));
+    col_slots[static_cast<size_t>(i)] = n;
+  }
+  const int slots_per_col = *std::max_element(col_slots.begin(), col_slots.end());
+  const long cSpart = 0, cSfin = cSpart + Tc * NB2, cArrive = cSfin + Tc;
+  P.counters = cArrive + static_cast<long>(N) * slots_per_col;
+  P.scratch_doubles = static_cast<size_t>(kRing) * slots_per_col * kB * kB;
   auto spart = [&](long s, int p, int q) { return static_cast<int>(cSpart + s * NB2 + p * nb + q); };
   auto sfin = [&](long s) { return static_cast<int>(cSfin + s); };
   auto cslot = [&](int i, int j) {
@@ -480,136 +507,133 @@ DataflowPlan build_phase2_dataflow(const Pattern& F, const Closure& sel, int cri
     return s;
   };
   auto final_count = [&](long s) { return C.tiles()[static_cast<size_t>(s)].i == C.tiles()[static_cast<size_t>(s)].j ? nb * (nb + 1) / 2 : NB2; };
-  P.slot_tiles = C.tiles();
-  Builder B(P);
+  // completion deps of every target of a column (ring-slot release)
+  std::vector<std::vector<Dep>> col_done(static_cast<size_t>(N));
   for (const ColumnWork& cw : sel.columns) {
     const int i = cw.col;
-    std::vector<int> K;
-    for (const int* r = F.rows_begin(i); r != F.rows_end(i); ++r)
-      if (*r > i) K.push_back(*r);
+    for (int j : cw.offdiag_rows) col_done[static_cast<size_t>(i)].push_back({sfin(cslot(j, i)), NB2});
+    if (cw.diagonal) col_done[static_cast<size_t>(i)].push_back({sfin(cslot(i, i)), nb * (nb + 1) / 2});
+  }
+  P.slot_tiles = C.tiles();
+  Builder B(P);
+  for (size_t ci = 0; ci < sel.columns.size(); ++ci) {
+    const ColumnWork& cw = sel.columns[ci];
+    const int i = cw.col;
+    const std::vector<int>& K = Kof[static_cast<size_t>(i)];
     const int kcrit = K.empty() ? -1 : K[0];
+    // ring release: the column processed kRing steps earlier must be complete
+    std::vector<Dep> ring_deps;
+    if (ci >= static_cast<size_t>(kRing)) ring_deps = col_done[static_cast<size_t>(sel.columns[ci - kRing].col)];
+    int slot_next = 0;
+    auto take = [&](int parts, DTask& t, int part, int base) {
+      t.kind = kSplitTask;
+      t.p_off = (static_cast<long long>(i % kRing) * slots_per_col + base) * kB * kB;
+      t.aux0 = static_cast<int>(cArrive + static_cast<long>(i) * slots_per_col + base);
+      t.aux1 = (part << 8) | parts;
+    };
     auto mseg = [&](DTask& t, int j, int k) {
       const long ms = cslot(std::max(j, k), std::min(j, k));
       B.seg(t, kStoreSigma, tile_off(ms, bp), kStoreP1, tile_off(F.slot(k, i), bp), 0, bp,
             (k > j ? kTransA : 0) | kNegate);
     };
-    struct Off {
-      int j;
-      long ts;
-      bool has_early, has_crit;
+    auto mdep = [&](int j, int k) {
+      const long ms = cslot(std::max(j, k), std::min(j, k));
+      return Dep{sfin(ms), final_count(ms)};
     };
-    std::vector<Off> offs;
+    // off-diagonal targets: Sigma_ji = -sum_k M_jk W_ki.  Terms whose M tile
+    // lies in column kcrit (the column processed just before) are late; the
+    // others (older columns) form one early task that runs ahead.
     for (int j : cw.offdiag_rows) {
-      Off o{j, cslot(j, i), false, false};
-      for (int k : K) (k == j ? o.has_crit : o.has_early) = true;
-      offs.push_back(o);
-    }
-    // early parts (and targets without a k == j term)
-    for (const Off& o : offs) {
-      if (!o.has_early) continue;
+      const long ts = cslot(j, i);
+      std::vector<int> early, late;
+      for (int k : K) (std::min(j, k) == kcrit ? late : early).push_back(k);
+      const int parts = static_cast<int>(late.size());
       for (int p = 0; p < nb; ++p)
         for (int q = 0; q < nb; ++q) {
-          std::vector<Dep> d;
-          for (int k : K)
-            if (k != o.j) {
-              const long ms = cslot(std::max(o.j, k), std::min(o.j, k));
-              d.push_back({sfin(ms), final_count(ms)});
-            }
-          std::sort(d.begin(), d.end(), [](const Dep& x, const Dep& y) { return x.counter < y.counter; });
-          d.erase(std::unique(d.begin(), d.end(), [](const Dep& x, const Dep& y) { return x.counter == y.counter; }),
-                  d.end());
-          DTask& t = B.add(1, d, {o.has_crit ? spart(o.ts, p, q) : sfin(o.ts)});
-          t.kind = kGemmTask;
-          t.c_store = kStoreSigma;
-          t.c_off = blk_off(o.ts, bp, p, q);
-          t.m0 = p * kB;
-          t.n0 = q * kB;
-          for (int k : K)
-            if (k != o.j) mseg(t, o.j, k);
-        }
-    }
-    auto emit_crit = [&](const Off& o, int queue) {
-      const long dj = cslot(o.j, o.j);
-      for (int p = 0; p < nb; ++p)
-        for (int q = 0; q < nb; ++q) {
-          std::vector<Dep> d{{sfin(dj), final_count(dj)}};
-          if (o.has_early) d.push_back({spart(o.ts, p, q), 1});
-          DTask& t = B.add(queue, d, {sfin(o.ts)});
-          t.kind = kGemmTask;
-          t.c_store = kStoreSigma;
-          t.c_off = blk_off(o.ts, bp, p, q);
-          if (o.has_early) {
-            t.c0_store = kStoreSigma;
-            t.c0_off = t.c_off;
+          if (!early.empty()) {
+            std::vector<Dep> d;
+            for (int k : early) d.push_back(mdep(j, k));
+            std::sort(d.begin(), d.end(), [](const Dep& x, const Dep& y) { return x.counter < y.counter; });
+            d.erase(std::unique(d.begin(), d.end(), [](const Dep& x, const Dep& y) { return x.counter == y.counter; }),
+                    d.end());
+            DTask& t = B.add(1, d, {late.empty() ? sfin(ts) : spart(ts, p, q)});
+            t.kind = kGemmTask;
+            t.c_store = kStoreSigma;
+            t.c_off = blk_off(ts, bp, p, q);
+            t.m0 = p * kB;
+            t.n0 = q * kB;
+            for (int k : early) mseg(t, j, k);
           }
-          t.m0 = p * kB;
-          t.n0 = q * kB;
-          mseg(t, o.j, o.j);
+          const int base = slot_next;
+          for (int r = 0; r < parts; ++r) {
+            std::vector<Dep> d{mdep(j, late[static_cast<size_t>(r)])};
+            std::vector<Dep> d2;
+            if (!early.empty()) d2.push_back({spart(ts, p, q), 1});
+            if (parts > 1) d.insert(d.end(), ring_deps.begin(), ring_deps.end());
+            else d.insert(d.end(), d2.begin(), d2.end());
+            DTask& t = B.add(1, d, {sfin(ts)}, parts > 1 ? d2 : std::vector<Dep>{});
+            t.kind = kGemmTask;
+            t.c_store = kStoreSigma;
+            t.c_off = blk_off(ts, bp, p, q);
+            if (!early.empty()) {
+              t.c0_store = kStoreSigma;
+              t.c0_off = t.c_off;
+            }
+            t.m0 = p * kB;
+            t.n0 = q * kB;
+            if (parts > 1) take(parts, t, r, base);
+            mseg(t, j, late[static_cast<size_t>(r)]);
+          }
+          if (parts > 1) slot_next += parts;
         }
-    };
-    for (const Off& o : offs)
-      if (o.has_crit && o.j != kcrit) emit_crit(o, 1);
+    }
+    // diagonal target: Sigma_ii = X_i^T X_i - sum_k W_ki^T Sigma_ki (LAUUM +
+    // one part per term, all depending on this column's off-diagonal tiles),
+    // lower part mirrored exactly, diagonal -> marginal variances.
     if (cw.diagonal) {
       const long dsl = cslot(i, i);
       const long xs = F.col_start(i);
-      const bool split = kcrit >= 0;
-      auto diag_task = [&](int p, int q, bool early) {
-        std::vector<Dep> d;
-        std::vector<int> sg;
-        if (early) {
-          for (int k : K)
-            if (k != kcrit) d.push_back({sfin(cslot(k, i)), NB2});
-          sg.push_back(spart(dsl, p, q));
-        } else {
-          if (split) {
-            d.push_back({spart(dsl, p, q), 1});
-            d.push_back({sfin(cslot(kcrit, i)), NB2});
-          }
-          sg.push_back(sfin(dsl));
-        }
-        DTask& t = B.add(early ? 1 : 0, d, sg);
-        t.kind = kGemmTask;
-        t.c_store = kStoreSigma;
-        t.c_off = blk_off(dsl, bp, p, q);
-        t.m0 = p * kB;
-        t.n0 = q * kB;
-        if (!early) {
-          if (split) {
-            t.c0_store = kStoreSigma;
-            t.c0_off = t.c_off;
-          }
-          if (p == q) {
-            t.mode = kSymDiag;
-            t.diag_store = kStoreVar;
-            t.diag_off = static_cast<long long>(i) * bp + p * kB;
-          } else {
-            t.mode = kMirror;
-            t.cm_store = kStoreSigma;
-            t.cm_off = blk_off(dsl, bp, q, p);
-          }
-        }
-        if (early || !split) {
-          // U U^T = X^T X; rows >= p*64 of X carry the nonzeros for block row p >= q
-          B.seg(t, kStoreP1, tile_off(xs, bp), kStoreP1, tile_off(xs, bp), p * kB, bp, kTransA);
-          for (int k : K)
-            if (k != kcrit || !split)
+      const int parts = 1 + static_cast<int>(K.size());
+      for (int p = 0; p < nb; ++p)
+        for (int q = 0; q <= p; ++q) {
+          const int base = slot_next;
+          for (int r = 0; r < parts; ++r) {
+            std::vector<Dep> d;
+            if (r == 0) {
+              // the LAUUM part runs when the column becomes active
+              if (kcrit >= 0 && C.slot(kcrit, kcrit) >= 0) d.push_back(mdep(kcrit, kcrit));
+            } else {
+              const long ks = cslot(K[static_cast<size_t>(r - 1)], i);
+              d.push_back({sfin(ks), NB2});
+            }
+            if (parts > 1) d.insert(d.end(), ring_deps.begin(), ring_deps.end());
+            DTask& t = B.add(0, d, {sfin(dsl)});
+            t.kind = kGemmTask;
+            t.c_store = kStoreSigma;
+            t.c_off = blk_off(dsl, bp, p, q);
+            t.m0 = p * kB;
+            t.n0 = q * kB;
+            if (p == q) {
+              t.mode = kSymDiag;
+              t.diag_store = kStoreVar;
+              t.diag_off = static_cast<long long>(i) * bp + p * kB;
+            } else {
+              t.mode = kMirror;
+              t.cm_store = kStoreSigma;
+              t.cm_off = blk_off(dsl, bp, q, p);
+            }
+            if (parts > 1) take(parts, t, r, base);
+            if (r == 0) {
+              // U U^T = X^T X; rows >= p*64 of X carry the nonzeros for block row p >= q
+              B.seg(t, kStoreP1, tile_off(xs, bp), kStoreP1, tile_off(xs, bp), p * kB, bp, kTransA);
+            } else {
+              const int k = K[static_cast<size_t>(r - 1)];
               B.seg(t, kStoreP1, tile_off(F.slot(k, i), bp), kStoreSigma, tile_off(cslot(k, i), bp), 0, bp,
                     kTransA | kNegate);
-        } else {
-          B.seg(t, kStoreP1, tile_off(F.slot(kcrit, i), bp), kStoreSigma, tile_off(cslot(kcrit, i), bp), 0, bp,
-                kTransA | kNegate);
+            }
+          }
+          if (parts > 1) slot_next += parts;
         }
-      };
-      if (split)
-        for (int p = 0; p < nb; ++p)
-          for (int q = 0; q <= p; ++q) diag_task(p, q, true);
-      for (const Off& o : offs)
-        if (o.has_crit && o.j == kcrit) emit_crit(o, 0);
-      for (int p = 0; p < nb; ++p)
-        for (int q = 0; q <= p; ++q) diag_task(p, q, false);
-    } else {
-      for (const Off& o : offs)
-        if (o.has_crit && o.j == kcrit) emit_crit(o, 0);
     }
   }
   B.finish(crit_workers);

@@ -161,7 +161,7 @@ def run_plans(tib, matrix, selection):
         2: np.zeros(len(fpat) * bp * bp),
         3: np.zeros(len(closure) * bp * bp),
         4: np.zeros(N * bp),
-        5: np.zeros(max(pf["scratch_doubles"], 1)),
+        5: np.zeros(max(pf["scratch_doubles"], pp["scratch_doubles"], 1)),
         6: np.zeros(N * nb),
     }
     status = [np.iinfo(np.int64).max]

@@ -28,17 +28,19 @@ STORE = {0: "A", 1: "L", 2: "P1", 3: "S", 5: "T", 255: "-"}
 
 def load(path):
     with open(path, "rb") as f:
-        hdr = np.frombuffer(f.read(80), np.int64)
-        if hdr[0] != -3:
+        hdr = np.frombuffer(f.read(88), np.int64)
+        if hdr[0] != -4:
             raise SystemExit(f"{path}: old trace format")
-        ntask, batch, nq0, nb, ndep, nsig, nseg, ntiles, bp = (int(x) for x in hdr[1:])
+        ntask, batch, nq0, nb, ndep, nsig, nseg, ntiles, bp, nchain = (int(x) for x in hdr[1:])
         tasks = np.frombuffer(f.read(DTASK.itemsize * ntask), DTASK)
         deps = np.frombuffer(f.read(8 * ndep), DEP)
         sigs = np.frombuffer(f.read(4 * nsig), np.int32)
         segs = np.frombuffer(f.read(32 * nseg), SEG)
         tiles = np.frombuffer(f.read(8 * ntiles), np.int32).reshape(-1, 2)
         rec = np.frombuffer(f.read(), np.uint64).reshape(-1, 4)
-    return dict(ntask=ntask, batch=batch, nq0=nq0, nb=nb, tasks=tasks, deps=deps, sigs=sigs, segs=segs, rec=rec,
+    chain = rec[ntask * batch:]
+    rec = rec[:ntask * batch]
+    return dict(chain=chain,ntask=ntask, batch=batch, nq0=nq0, nb=nb, tasks=tasks, deps=deps, sigs=sigs, segs=segs, rec=rec,
                 tiles=tiles, bp=bp)
 
 
@@ -74,6 +76,29 @@ def label(t, q0):
     return f"{q}:{name}/s{int(t['seg_count'])}{sp}"
 
 
+def chain_report(d, t0):
+    ch = d["chain"].astype(np.float64) / 1e3
+    if len(ch) == 0:
+        return
+    ok = ch[:, 0] > 0
+    ch = ch[ok] - t0
+    start, met, core, fat = ch[:, 0], ch[:, 1], ch[:, 2], ch[:, 3]
+    n = len(ch)
+    dep_wait = met - start
+    core_t = core - met
+    fat_wait = np.where(fat > 0, fat - core, 0)
+    nxt = np.append(start[1:], np.nan)
+    tail = nxt - core  # from core done (and fat) to the next step start
+    print(f"  chain: {n} steps over {start[0]:.1f}..{core[-1]:.1f} us")
+    print(f"    per step mean: dep wait {dep_wait.mean():.2f} us, leaf core {core_t.mean():.2f} (p50 {np.median(core_t):.2f}), "
+          f"fat-phase wait {fat_wait.mean():.2f}, fat+rest {np.nanmean(tail - fat_wait):.2f}; step {np.nanmean(nxt - start):.2f} us")
+    nb = d["nb"]
+    first = np.arange(n) % nb == 0
+    if first.any():
+        print(f"    tile-first steps: dep wait mean {dep_wait[first].mean():.2f} us (total {dep_wait[first].sum() / 1e3:.1f} ms); "
+              f"other steps dep wait total {dep_wait[~first].sum() / 1e3:.1f} ms, fat waits total {fat_wait.sum() / 1e3:.1f} ms")
+
+
 def report(path):
     d = load(path)
     tasks, deps, sigs, rec, batch, nq0 = d["tasks"], d["deps"], d["sigs"], d["rec"], d["batch"], d["nq0"]
@@ -93,6 +118,7 @@ def report(path):
     labels = np.array([label(tasks[i], i < nq0) for i in range(len(tasks))])
     lab = labels[tidx]
     print(f"{path}: tasks={len(rec)} (q0 {q0.sum()}, q1 {(~q0).sum()}) batch={batch} span={span:.1f} us")
+    chain_report(d, t0 / 1e0)
     nsm = len(np.unique(sm))
     busy_all = (done - ready).sum()
     print(f"  CTA-busy fraction {busy_all / (span * 2 * nsm):.3f} (2 CTAs x {nsm} SMs)")
