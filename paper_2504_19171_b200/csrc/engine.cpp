@@ -404,6 +404,26 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
     launch_zero_strips(P.zero.p, static_cast<int>(P.zero.n), P.host.bp, batch, e.tables, s);
     launch_dataflow(a, P.need.p, P.init0.p, static_cast<int>(P.init0.n), P.init1.p, static_cast<int>(P.init1.n), P.grid, s);
   };
+  if (std::getenv("TIB_CHAIN_PROF") && set_chain_profile(nullptr) == cudaSuccess) {
+    // phases: 0 chol32 A00, 1 coupling DMMA, 2 chol32 A11, 3 X10 DMMA, 4 logdet + stores,
+    // 5 phase-1 signals, 6 second-phase wait, 7 fat part, 8 phase-2 signals, 9 step dependency wait
+    long long* prof = nullptr;
+    CK(cudaMalloc(reinterpret_cast<void**>(&prof), 16 * sizeof(long long)));
+    CK(cudaMemsetAsync(prof, 0, 16 * sizeof(long long), s));
+    CK(static_cast<cudaError_t>(set_chain_profile(prof)));
+    enqueue();
+    CK(cudaGetLastError());
+    long long h[16];
+    CK(cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    CK(static_cast<cudaError_t>(set_chain_profile(nullptr)));
+    cudaFree(prof);
+    const double n = static_cast<double>(std::max<size_t>(P.host.chain.size(), 1)) * batch;
+    std::fprintf(stderr, "chain profile (cycles per step):");
+    for (int i = 0; i < 10; ++i) std::fprintf(stderr, " p%d=%.0f", i, h[i] / n);
+    std::fprintf(stderr, "\n");
+    return;
+  }
   if (trace_prefix()) {
     unsigned long long* d_trace = nullptr;
     const size_t n = (nt + P.host.chain.size()) * batch * 4;
@@ -1160,7 +1180,10 @@ int tib_resident_info(tib_resident r, double* model, double* executed, double* l
     if (model) *model = r->model_flops;
     if (executed) *executed = r->fp->flow->host.task_flops + r->p2->flow->host.task_flops;
     if (logdet) *logdet = r->logdet;
-    if (launches) *launches = 2;  // one persistent dataflow kernel per sweep
+    // per sweep: scheduler init + the persistent dataflow kernel (+ the zero-strip
+    // kernel when the plan has strips)
+    if (launches)
+      *launches = 4 + (r->fp->flow->host.zero.empty() ? 0 : 1) + (r->p2->flow->host.zero.empty() ? 0 : 1);
   });
 }
 

@@ -39,6 +39,9 @@ struct FlowArgs {
   unsigned long long* trace;
 };
 
+// Chain phase profile accumulator (16 long longs of device memory) or null.
+int set_chain_profile(long long* p);
+
 void launch_dataflow(const FlowArgs& a, const int* need, const int* init0, int n_init0, const int* init1, int n_init1,
                      int grid, cudaStream_t s);
 void launch_zero_strips(const ZeroStrip* z, int count, int ld, int batch, const BaseTable* tables, cudaStream_t s);

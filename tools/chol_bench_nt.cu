@@ -1,7 +1,6 @@
 // Microbenchmark of the warp-level 32x32 Cholesky + inverse (chol32_warp) and
 // the 64x64 leaf in isolation: one CTA, clock64 stamps.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../paper_2504_19171_b200/csrc chol_bench.cu -o chol_bench
-
 #include "../paper_2504_19171_b200/csrc/kernels.cu"
 #include <cstdio>
 #include <vector>
@@ -141,6 +140,7 @@ int main() {
     cudaMemcpy(cc, cyc, 24, cudaMemcpyDeviceToHost);
     printf("{\"leafT_chol_a\": %lld, \"dmma\": %lld, \"chol_b\": %lld}\n", cc[0], cc[1], cc[2]);
   }
+  long long* prof; cudaMalloc(&prof, 128); cudaMemset(prof, 0, 128); set_chain_profile(prof);
   for (int it = 0; it < 3; ++it) {
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
@@ -150,6 +150,8 @@ int main() {
     cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
     printf("{\"leaf_cycles\": %lld, \"us_per_leaf\": %.2f, \"err\": \"%s\"}\n", c, ms * 1000 / 20, cudaGetErrorString(cudaGetLastError()));
   }
+  { long long h[16]; cudaMemcpy(h, prof, 128, cudaMemcpyDeviceToHost);
+    printf("{\"prof_per_leaf\": [%lld, %lld, %lld, %lld, %lld]}\n", h[0]/60, h[1]/60, h[2]/60, h[3]/60, h[4]/60); }
   std::vector<double> l(64 * 64), x(64 * 64);
   cudaMemcpy(l.data(), dL, 64 * 64 * 8, cudaMemcpyDeviceToHost);
   cudaMemcpy(x.data(), dX, 64 * 64 * 8, cudaMemcpyDeviceToHost);
