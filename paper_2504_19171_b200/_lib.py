@@ -10,7 +10,9 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtileinv_b200.so")
+# TIB_LIB_VARIANT=prof selects the profiling build (make -C csrc prof: -DTIB_PROF)
+_VARIANT = os.environ.get("TIB_LIB_VARIANT", "")
+LIB_PATH = os.path.join(_HERE, f"libtileinv_b200{'_' + _VARIANT if _VARIANT else ''}.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

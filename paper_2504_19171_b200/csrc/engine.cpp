@@ -292,7 +292,8 @@ static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int 
   plan->sym = symbolic_cholesky(pattern);
   plan->L = plan->sym.filled.layout();
   plan->flow = upload_plan(build_factor_dataflow(plan->sym.filled, crit_workers(), env_int("TIB_DEFER_W", 2),
-                                                  env_int("TIB_FAT_LEAF", 0) != 0, env_int("TIB_CHAIN", 1) != 0),
+                                                  env_int("TIB_FAT_LEAF", 0) != 0, env_int("TIB_CHAIN", 1) != 0,
+                                                  env_int("TIB_CHAIN", 1) != 0 && env_int("TIB_BOUNDARY", 1) != 0),
                            device, s);
   plan->bp = plan->flow->host.bp;
   plan->nb = plan->flow->host.nb;
@@ -405,8 +406,9 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
     launch_dataflow(a, P.need.p, P.init0.p, static_cast<int>(P.init0.n), P.init1.p, static_cast<int>(P.init1.n), P.grid, s);
   };
   if (std::getenv("TIB_CHAIN_PROF") && set_chain_profile(nullptr) == cudaSuccess) {
-    // phases: 0 chol32 A00, 1 coupling DMMA, 2 chol32 A11, 3 X10 DMMA, 4 logdet + stores,
-    // 5 phase-1 signals, 6 second-phase wait, 7 fat part, 8 phase-2 signals, 9 step dependency wait
+    // phases: 0 leaf (10 chol32 A00, 11 coupling DMMA, 12 chol32 A11, 13 X10 DMMA, rest: logdet + stores),
+    // 5 phase-1 signals, 6 second-phase wait + operand prefetch issue, 7 fat part, 8 phase-2 signals,
+    // 9 step dependency wait
     long long* prof = nullptr;
     CK(cudaMalloc(reinterpret_cast<void**>(&prof), 16 * sizeof(long long)));
     CK(cudaMemsetAsync(prof, 0, 16 * sizeof(long long), s));
@@ -420,7 +422,7 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
     cudaFree(prof);
     const double n = static_cast<double>(std::max<size_t>(P.host.chain.size(), 1)) * batch;
     std::fprintf(stderr, "chain profile (cycles per step):");
-    for (int i = 0; i < 10; ++i) std::fprintf(stderr, " p%d=%.0f", i, h[i] / n);
+    for (int i = 0; i < 16; ++i) std::fprintf(stderr, " p%d=%.0f", i, h[i] / n);
     std::fprintf(stderr, "\n");
     return;
   }
@@ -1069,7 +1071,10 @@ int tib_plan_export(tib_matrix m, int preset, const long* rows, const long* cols
     const FactorPlan sym = symbolic_cholesky(m->pattern);
     DataflowPlan P;
     if (which == 0) {
-      P = build_factor_dataflow(sym.filled, crit_workers, env_int("TIB_DEFER_W", 2), env_int("TIB_FAT_LEAF", 0) != 0);
+      // the CPU simulator runs the same decomposition as the GPU chain, with the
+      // chain's steps kept as (fat / boundary) leaf tasks
+      P = build_factor_dataflow(sym.filled, crit_workers, env_int("TIB_DEFER_W", 2), env_int("TIB_FAT_LEAF", 0) != 0,
+                                false, env_int("TIB_CHAIN", 1) != 0 && env_int("TIB_BOUNDARY", 1) != 0);
     } else {
       const Closure sel =
           symbolic_inversion(select_tiles(sym.filled.layout(), sym.filled, make_request(preset, rows, cols, ne)), sym.filled);

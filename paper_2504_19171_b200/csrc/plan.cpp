@@ -170,8 +170,10 @@ void validate_dataflow(const DataflowPlan& plan, const std::vector<int>& order) 
   }
 }
 
-DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer_w, bool fat_leaf, bool chain) {
+DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer_w, bool fat_leaf, bool chain,
+                                   bool boundary) {
   if (chain) fat_leaf = true;
+  if (boundary) fat_leaf = true;
   DataflowPlan P;
   P.L = F.layout();
   const Layout& L = P.L;
@@ -189,13 +191,19 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
   for (int q = 0; q < nb; ++q)
     if (panel_parts(q) > 1) panel_slots += nb * panel_parts(q);
   const int upd_slots = upd_parts > 1 ? NB2 * upd_parts : 0;
-  const int slots_per_col = 2 * panel_slots + 2 * upd_slots;
+  // tile-boundary trick (boundary && nb >= 2): per row p of the first tile,
+  // S_p = sum_{k < nb-1} A(k0, j)[p, k] T(nb-1, k)^T split over parts of <= 128,
+  // plus the reduced S_p block itself
+  const bool bnd = boundary && nb >= 2;
+  const int s_parts = bnd ? (nb - 1 + 1) / 2 : 0;
+  const int s_slots = bnd ? nb * (s_parts > 1 ? s_parts : 0) + nb : 0;
+  const int slots_per_col = 2 * panel_slots + 2 * upd_slots + s_slots;
   constexpr int kRing = 4;  // columns of partial slots in flight (see the reuse argument below)
   // counter spaces
   const long cAord = 0, cAfin = cAord + T * NB2, cLblk = cAfin + T, cLfin = cLblk + T * NB2,
              cXblk = cLfin + T, cXfin = cXblk + static_cast<long>(N) * NB2, cTblk = cXfin + N,
              cWfin = cTblk + static_cast<long>(N) * NB2, cXrow = cWfin + T, cArrive = cXrow + static_cast<long>(N) * nb,
-             cEnd = cArrive + static_cast<long>(N) * slots_per_col;
+             cSdone = cArrive + static_cast<long>(N) * slots_per_col, cEnd = cSdone + static_cast<long>(N) * nb;
   P.counters = cEnd;
   const size_t t_doubles = static_cast<size_t>(N) * bp * bp;
   P.scratch_doubles = t_doubles + static_cast<size_t>(kRing) * slots_per_col * kB * kB;
@@ -209,6 +217,7 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
   auto tcnt = [&](int j, int p, int q) { return static_cast<int>(cTblk + static_cast<long>(j) * NB2 + p * nb + q); };
   auto wfin = [&](long s) { return static_cast<int>(cWfin + s); };
   auto xrowc = [&](int j, int q) { return static_cast<int>(cXrow + static_cast<long>(j) * nb + q); };
+  auto sdone = [&](int j, int p) { return static_cast<int>(cSdone + static_cast<long>(j) * nb + p); };
   const int xdone = nb * (nb + 1) / 2;
   const long long tsz = static_cast<long long>(bp) * bp;
 
@@ -245,6 +254,21 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
         krows.push_back(*r);
         ks.push_back(F.slot(*r, j));
       }
+    // first off-diagonal tile of the column and its update ordinals (the
+    // progressive tail below), needed by the boundary leaf
+    const bool tail0 = !krows.empty(), tail1 = krows.size() > 1;
+    const long sk0 = tail0 ? ks[0] : -1;
+    const long ts00 = tail0 ? F.slot(krows[0], krows[0]) : -1;
+    const int Uk0 = tail0 ? ord[static_cast<size_t>(sk0)] : 0;
+    int u00 = 0, u10 = 0;
+    if (tail0) u00 = ord[static_cast<size_t>(ts00)]++;
+    if (tail1) u10 = ord[static_cast<size_t>(F.slot(krows[1], krows[0]))]++;
+    const bool bnd_col = bnd && tail0;
+    auto s_off = [&](int p) {  // reduced S_p block of this column (ring slot)
+      return static_cast<long long>(t_doubles) +
+             (static_cast<long long>(j % kRing) * slots_per_col + 2 * panel_slots + 2 * upd_slots + nb * (s_parts > 1 ? s_parts : 0) + p) *
+                 kB * kB;
+    };
     // ---- diagonal-tile chain (queue 0): blocked POTRF + TRTRI of tile (j, j)
     // Fat leaf: factor + invert block (kk, kk), then (kk + 1 < nb, after the
     // second-phase dependencies) the next panel block L(kk+1, kk) = A(kk+1, kk)
@@ -253,17 +277,43 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
       std::vector<Dep> d{{aord(ds, kk, kk), U + kk}}, d2;
       std::vector<int> sg{lblk(ds, kk, kk), lfin(ds), xblk(j, kk, kk), xfin(j), xrowc(j, kk)};
       const bool fat = fat_leaf && kk + 1 < nb;
+      // boundary leaf (last block of the tile): its second phase forms row 0 of
+      // the first off-diagonal tile's last block column, L(k0, j)[0, nb-1] =
+      // (A(k0, j)[0, nb-1] - S_0) X_{nb-1}^T, and the last update term of block
+      // (0, 0) of tile (k0, k0) -- the next chain step's block
+      const bool bleaf = bnd_col && kk == nb - 1;
       if (fat) {
         d2.push_back({aord(ds, kk + 1, kk), U + kk});
         d2.push_back({aord(ds, kk + 1, kk + 1), U + kk});
         sg.push_back(lblk(ds, kk + 1, kk));
         sg.push_back(lfin(ds));
         sg.push_back(aord(ds, kk + 1, kk + 1));
+      } else if (bleaf) {
+        d2.push_back({sdone(j, 0), 1});
+        d2.push_back({afin(sk0), Uk0 * NB2});
+        d2.push_back({aord(ts00, 0, 0), u00 + 1});
+        sg.push_back(lblk(sk0, 0, nb - 1));
+        sg.push_back(lfin(sk0));
+        sg.push_back(aord(ts00, 0, 0));
       }
       DTask& t = B.add(0, d, sg, d2);
-      t.sig2_count = fat ? 3 : 0;
+      t.sig2_count = (fat || bleaf) ? 3 : 0;
       t.kind = kLeafTask;
-      t.mode = fat ? 2 : 0;
+      t.mode = fat ? 2 : (bleaf ? 4 : 0);
+      if (bleaf) {
+        t.p_off = blk_off(sk0, bp, 0, nb - 1);  // P in the A store; L(k0, j)[0, nb-1] at the same offset in L
+        Seg sgx{};
+        sgx.a_store = kStoreScratch;
+        sgx.a_off = s_off(0);                    // S_0
+        sgx.b_store = kStoreA;
+        sgx.b_off = blk_off(ts00, bp, 0, 0);     // next diagonal block
+        sgx.lda = kB;  // S_0 is a 64x64 block
+        sgx.ldb = bp;
+        t.seg_begin = static_cast<int>(P.segs.size());
+        t.seg_count = 1;
+        P.segs.push_back(sgx);
+        P.task_flops += 2.0 * kB * kB * kB * 2;
+      }
       t.c_off = t.c0_off = t.cm_off = blk_off(ds, bp, kk, kk);
       t.diag_off = static_cast<long long>(j) * nb + kk;
       t.m0 = valid - kk * kB;
@@ -343,24 +393,33 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
       }
     };
     // k-blocks [2r, 2r + 2) of the update of tile (krows[ia], krows[ic]); u = its ordinal
-    auto update_split = [&](size_t ia, size_t ic, int r, int u, int queue, int slot_base) {
+    // which: 0 every block, 1 all but block (0, 0), 2 only block (0, 0).  With
+    // the boundary trick, block (0, 0) of tile (k0, k0) takes k < nb-1 only (the
+    // chain applies the last term), so its parts are clipped and counted apart.
+    auto update_split = [&](size_t ia, size_t ic, int r, int u, int queue, int slot_base, int which = 0) {
       const int a = krows[ia], c = krows[ic];
       const long ts = F.slot(a, c);
       if (ts < 0) throw Error(kErrConsistency, "update target outside the filled pattern");
-      const int klo = upd_parts > 1 ? 2 * r : 0, khi = upd_parts > 1 ? std::min(nb, 2 * r + 2) : nb;
       for (int p = 0; p < nb; ++p)
         for (int q = 0; q < (a == c ? p + 1 : nb); ++q) {
+          const bool b00 = p == 0 && q == 0;
+          if ((which == 1 && b00) || (which == 2 && !b00)) continue;
+          const bool clip = bnd_col && ia == 0 && ic == 0 && b00;
+          const int kend = clip ? nb - 1 : nb;
+          const int klo = upd_parts > 1 ? 2 * r : 0, khi = upd_parts > 1 ? std::min(kend, 2 * r + 2) : kend;
+          if (khi <= klo) continue;
+          const int parts = upd_parts > 1 ? (clip ? nb / 2 : upd_parts) : 1;
           std::vector<Dep> d;
           for (int k = klo; k < khi; ++k) {
             d.push_back({lblk(ks[ia], p, k), 1});
             if (!(ia == ic && q == p)) d.push_back({lblk(ks[ic], q, k), 1});
           }
           std::vector<Dep> d2{{aord(ts, p, q), u}};
-          if (upd_parts == 1) d.insert(d.end(), d2.begin(), d2.end());
+          if (parts == 1) d.insert(d.end(), d2.begin(), d2.end());
           std::vector<int> sg{aord(ts, p, q)};
           if (a != c) sg.push_back(afin(ts));
-          DTask& t = B.add(queue, d, sg, upd_parts > 1 ? d2 : std::vector<Dep>{});
-          t.kind = upd_parts > 1 ? kSplitTask : kGemmTask;
+          DTask& t = B.add(queue, d, sg, parts > 1 ? d2 : std::vector<Dep>{});
+          t.kind = parts > 1 ? kSplitTask : kGemmTask;
           t.c_store = t.c0_store = kStoreA;
           t.c_off = t.c0_off = blk_off(ts, bp, p, q);
           t.m0 = p * kB;
@@ -372,22 +431,71 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
             t.p_off = static_cast<long long>(t_doubles) +
                       (static_cast<long long>(j % kRing) * slots_per_col + slot) * kB * kB;
             t.aux0 = static_cast<int>(cArrive + static_cast<long>(j) * slots_per_col + slot);
-            t.aux1 = (r << 8) | upd_parts;
+            t.aux1 = (r << 8) | parts;
+            if (parts == 1) t.kind = kGemmTask;
           }
           B.seg(t, kStoreL, tile_off(ks[ia], bp), kStoreL, tile_off(ks[ic], bp), klo * kB, khi * kB,
                 kTransB | kNegate);
         }
     };
-    const bool tail0 = !krows.empty(), tail1 = krows.size() > 1;
-    int u00 = 0, u10 = 0;
-    if (tail0) u00 = ord[static_cast<size_t>(F.slot(krows[0], krows[0]))]++;
-    if (tail1) u10 = ord[static_cast<size_t>(F.slot(krows[1], krows[0]))]++;
     const int upd_step_parts = upd_parts;  // parts issued at chain steps kk = 1, 3, 5, ... and nb - 1
     auto upd_part_at = [&](int kk) {
       if (upd_step_parts > 1) return (kk % 2 == 1 || kk == nb - 1) ? kk / 2 : -1;
       return kk == nb - 1 ? 0 : -1;
     };
 
+    // S_p = sum_{k < nb-1} A(k0, j)[p, k] T(nb-1, k)^T (split-K over parts of <= 128);
+    // ready once row nb-1 of T is accumulated, i.e. during the chain's last leaf
+    auto s_tasks = [&]() {
+      const int K = (nb - 1) * kB;
+      for (int p = 0; p < nb; ++p) {
+        for (int r = 0; r < s_parts; ++r) {
+          const int klo = s_parts > 1 ? r * 2 * kB : 0, khi = s_parts > 1 ? std::min(K, (r + 1) * 2 * kB) : K;
+          std::vector<Dep> d{{afin(sk0), Uk0 * NB2}};
+          for (int k = klo / kB; k < khi / kB; ++k) d.push_back({tcnt(j, nb - 1, k), nb - 1 - k});
+          DTask& t = B.add(0, d, {sdone(j, p)});
+          t.kind = s_parts > 1 ? kSplitTask : kGemmTask;
+          t.c_store = kStoreScratch;
+          t.c_off = s_off(p);
+          t.ldc = kB;
+          if (s_parts > 1) {
+            const int slot = 2 * panel_slots + 2 * upd_slots + p * s_parts;
+            t.p_off = static_cast<long long>(t_doubles) +
+                      (static_cast<long long>(j % kRing) * slots_per_col + slot) * kB * kB;
+            t.aux0 = static_cast<int>(cArrive + static_cast<long>(j) * slots_per_col + slot);
+            t.aux1 = (r << 8) | s_parts;
+          }
+          for (int k = klo / kB; k < khi / kB; ++k)
+            B.seg(t, kStoreA, blk_off(sk0, bp, p, k), kStoreScratch,
+                  tsz * j + static_cast<long long>(nb - 1) * kB * bp + k * kB, 0, kB, kTransB);
+        }
+      }
+    };
+    // L(k0, j)[p, nb-1] = (A(k0, j)[p, nb-1] - S_p) X_{nb-1}^T for rows p >= 1 (row 0: the chain)
+    auto last_panel = [&]() {
+      const long long xd = blk_off(ds, bp, nb - 1, nb - 1);
+      for (int p = 1; p < nb; ++p) {
+        DTask& t = B.add(0, {{xblk(j, nb - 1, nb - 1), 1}, {sdone(j, p), 1}, {afin(sk0), Uk0 * NB2}},
+                         {lblk(sk0, p, nb - 1), lfin(sk0)});
+        t.kind = kGemmTask;
+        t.c_store = kStoreL;
+        t.c_off = blk_off(sk0, bp, p, nb - 1);
+        B.seg(t, kStoreA, blk_off(sk0, bp, p, nb - 1), kStoreP1, xd, 0, kB, kTransB);
+        Seg& sg = P.segs.emplace_back();
+        sg = Seg{};
+        sg.a_store = kStoreScratch;
+        sg.a_off = s_off(p);
+        sg.lda = kB;
+        sg.b_store = kStoreP1;
+        sg.b_off = xd;
+        sg.ldb = bp;
+        sg.k_lo = 0;
+        sg.k_hi = kB;
+        sg.flags = kTransB | kNegate;
+        ++t.seg_count;
+        P.task_flops += 2.0 * kB * kB * kB;
+      }
+    };
     for (int kk = 0; kk < nb; ++kk) {
       leaf(kk);
       if (kk + 1 < nb && !fat_leaf) {
@@ -402,10 +510,25 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
           if (!(i == kk + 1 && p == kk + 1)) traild(i, p, kk);
       for (int kk2 = kk + 2; kk2 < nb; ++kk2)
         for (int k = 0; k <= kk; ++k) tterm(kk2, k, kk);
-      if (tail0) {
+      if (tail0 && !bnd_col) {
         panel_prog(0, kk, 0, 0);
         const int r = upd_part_at(kk);
         if (r >= 0) update_split(0, 0, r, u00, 0, 2 * panel_slots);
+      } else if (tail0) {
+        if (kk < nb - 1) panel_prog(0, kk, 0, 0);
+        else last_panel();
+        const int r = upd_part_at(kk);
+        if (r >= 0) update_split(0, 0, r, u00, 0, 2 * panel_slots, 1);
+        // block (0, 0): its clipped last part goes out one step early
+        if (upd_parts > 1) {
+          for (int rr = 0; rr < upd_parts; ++rr) {
+            const int last = std::min(nb - 1, 2 * rr + 2) - 1;
+            if (2 * rr < nb - 1 && last == kk) update_split(0, 0, rr, u00, 0, 2 * panel_slots, 2);
+          }
+        } else if (kk == nb - 2) {
+          update_split(0, 0, 0, u00, 0, 2 * panel_slots, 2);
+        }
+        if (kk == nb - 2) s_tasks();
       }
     }
     if (tail1) {

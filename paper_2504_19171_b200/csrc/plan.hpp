@@ -47,8 +47,10 @@ struct DataflowPlan {
 // column first) and deferred W_kj = L_kj X_j on queue 1.
 // fat_leaf fuses the next panel block and diagonal-block update into the leaf task.
 // chain: the leaves (fat) become the steps of one persistent chain task per matrix.
+// boundary: the last leaf of each tile also forms row 0 of the next tile's last
+// panel block and the last update term of the next diagonal block (S trick).
 DataflowPlan build_factor_dataflow(const Pattern& filled, int crit_workers, int defer_w, bool fat_leaf,
-                                   bool chain = false);
+                                   bool chain = false, bool boundary = false);
 
 // Phase 2 over a closure: per column descending, off-diagonal targets split
 // into an early part and the k == j term, diagonal targets into LAUUM + early

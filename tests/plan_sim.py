@@ -92,10 +92,10 @@ class Sim:
     def leaf(self, t):
         ld = int(t["ldc"])
         A = view(self.s[K_STORE["A"]], int(t["c_off"]), BLK, BLK, int(t["ldc0"]))
-        Lv = view(self.s[K_STORE["L"]], int(t["c0_off"]), BLK, BLK + BLK * int(t["seg_count"]), ld)
-        Xv = view(self.s[K_STORE["P1"]], int(t["cm_off"]), BLK, BLK + BLK * int(t["seg_count"]), ld)
-        Lv[:, BLK:] = 0.0
-        Xv[:, BLK:] = 0.0
+        # (the upper blocks of the diagonal tiles are cleared by the zero-strip
+        # kernel on the GPU; the simulator's stores start zeroed)
+        Lv = view(self.s[K_STORE["L"]], int(t["c0_off"]), BLK, BLK, ld)
+        Xv = view(self.s[K_STORE["P1"]], int(t["cm_off"]), BLK, BLK, ld)
         a = np.tril(A)
         a = a + np.tril(a, -1).T
         valid = int(t["m0"])
@@ -110,6 +110,14 @@ class Sim:
         Lv[:, :BLK] = np.tril(L)
         Xv[:, :BLK] = np.tril(X)
         self.s[K_STORE["LOGDET"]][int(t["diag_off"])] = np.sum(np.log(np.diag(L)[: max(0, valid)]))
+        if t["mode"] & 4:  # tile-boundary leaf: (P - S_0) X^T and the next diagonal block's last term
+            g = self.p["segs"][int(t["seg_begin"])]
+            S = view(self.s[int(g["a_store"])], int(g["a_off"]), BLK, BLK, int(g["lda"]))
+            P = view(self.s[K_STORE["A"]], int(t["p_off"]), BLK, BLK, ld)
+            Lp = (P - S) @ np.tril(X).T
+            view(self.s[K_STORE["L"]], int(t["p_off"]), BLK, BLK, ld)[:] = Lp
+            D = view(self.s[int(g["b_store"])], int(g["b_off"]), BLK, BLK, ld)
+            D[:] = D - np.tril(Lp @ Lp.T)
         if t["mode"] & 2:  # fat leaf: next panel block and diagonal update
             P = view(self.s[K_STORE["A"]], int(t["c_off"]) + BLK * ld, BLK, BLK, ld)
             Lp = P @ np.tril(X).T

@@ -1,0 +1,75 @@
+// Microbenchmark of the chain step in isolation (one CTA, no scheduler):
+// leaf (Cholesky + inverse of the carried 64x64 block) + the fat second phase
+// (next panel block, next diagonal update), repeated.  Variants time the leaf
+// alone with and without the global load, to compare with the in-sweep step.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../paper_2504_19171_b200/csrc chain_bench.cu -o chain_bench
+#include "../paper_2504_19171_b200/csrc/kernels.cu"
+#include <cstdio>
+#include <vector>
+using namespace tib;
+
+// mode 0: leaf with global load; 1: leaf on the carried block (reload SA from a
+// copy first, outside the timed region); 2: leaf + fat (full chain step)
+__global__ void chain_kernel(const double* A, const double* P, const double* Dn, double* L, double* X, double* Pout,
+                             DevStatus* st, double* ld, long long* cyc, int steps, int mode) {
+  extern __shared__ __align__(16) double smem[];
+  long long total = 0, leaf_t = 0;
+  for (int s = 0; s < steps; ++s) {
+    if (mode != 0) {
+      for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) smem[(i / 64) * kLs + i % 64] = (i % 64 <= i / 64) ? A[i] : 0.0;
+      __syncthreads();
+    }
+    const long long t0 = clock64();
+    leaf_potrf_inv<true>(mode == 0 ? A : nullptr, 64, L, X, 64, 64, 0, st, ld, smem);
+    const long long t1 = clock64();
+    if (mode == 2) {
+      chain_fat(P, Pout, Dn, 64, smem);
+      __syncthreads();
+    }
+    if (mode == 3) {
+      // code pollution: a block GEMM task between steps (like the sweep kernel's other paths)
+      RSeg sg{P, Dn, 64, 64, 0, 64, kTransB, 0};
+      RTask t{};
+      t.C = Pout;
+      t.ldc = t.ldc0 = 64;
+      t.seg_count = 1;
+      t.mode = kFull;
+      gemm_task(t, LocalSegs{&sg, 1}, smem);
+      chain_fat(P, Pout, Dn, 64, smem);
+      __syncthreads();
+    }
+    const long long t2 = clock64();
+    total += t2 - t0;
+    leaf_t += t1 - t0;
+  }
+  if (threadIdx.x == 0) {
+    cyc[0] = total / steps;
+    cyc[1] = leaf_t / steps;
+  }
+}
+
+int main() {
+  std::vector<double> a(64 * 64), p(64 * 64);
+  for (int i = 0; i < 64; ++i)
+    for (int j = 0; j < 64; ++j) {
+      a[i * 64 + j] = (i == j) ? 70.0 : 1.0 / (1 + i + j);
+      p[i * 64 + j] = 0.01 * ((i * 7 + j * 3) % 11 - 5);
+    }
+  double *dA, *dP, *dL, *dX, *dPo, *dld;
+  DevStatus* st;
+  long long* cyc;
+  cudaMalloc(&dA, 32768); cudaMalloc(&dP, 32768); cudaMalloc(&dL, 32768); cudaMalloc(&dX, 32768);
+  cudaMalloc(&dPo, 32768); cudaMalloc(&dld, 8); cudaMalloc(&st, 8); cudaMalloc(&cyc, 16);
+  cudaMemcpy(dA, a.data(), 32768, cudaMemcpyHostToDevice);
+  cudaMemcpy(dP, p.data(), 32768, cudaMemcpyHostToDevice);
+  cudaMemset(st, 0xff, 8);
+  cudaFuncSetAttribute(chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFlowSmemBytes);
+  for (int mode : {1, 1, 1}) {
+    chain_kernel<<<1, 128, kFlowSmemBytes>>>(dA, dP, dA, dL, dX, dPo, st, dld, cyc, 50, mode);
+    long long c[2];
+    cudaMemcpy(c, cyc, 16, cudaMemcpyDeviceToHost);
+    printf("{\"mode\": %d, \"step_cycles\": %lld, \"leaf_cycles\": %lld, \"err\": \"%s\"}\n", mode, c[0], c[1],
+           cudaGetErrorString(cudaGetLastError()));
+  }
+  return 0;
+}

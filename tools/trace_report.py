@@ -11,9 +11,9 @@ import numpy as np
 DTASK = np.dtype({
     "names": ["c_off", "c0_off", "cm_off", "diag_off", "p_off", "ldc", "ldc0", "m0", "n0", "seg_begin", "seg_count",
               "dep_begin", "sig_begin", "aux0", "aux1", "dep_count", "sig_count", "kind", "mode", "c_store",
-              "c0_store", "cm_store", "diag_store", "dep2_count"],
-    "formats": ["<i8"] * 5 + ["<i4"] * 10 + ["<u2"] * 2 + ["u1"] * 7,
-    "offsets": [0, 8, 16, 24, 32, 40, 44, 48, 52, 56, 60, 64, 68, 72, 76, 80, 82, 84, 85, 86, 87, 88, 89, 90],
+              "c0_store", "cm_store", "diag_store", "dep2_count", "sig2_count"],
+    "formats": ["<i8"] * 5 + ["<i4"] * 10 + ["<u2"] * 2 + ["u1"] * 8,
+    "offsets": [0, 8, 16, 24, 32, 40, 44, 48, 52, 56, 60, 64, 68, 72, 76, 80, 82, 84, 85, 86, 87, 88, 89, 90, 91],
     "itemsize": 96,
 })
 DEP = np.dtype([("counter", "<i4"), ("value", "<i4")])
@@ -92,6 +92,9 @@ def chain_report(d, t0):
     print(f"  chain: {n} steps over {start[0]:.1f}..{core[-1]:.1f} us")
     print(f"    per step mean: dep wait {dep_wait.mean():.2f} us, leaf core {core_t.mean():.2f} (p50 {np.median(core_t):.2f}), "
           f"fat-phase wait {fat_wait.mean():.2f}, fat+rest {np.nanmean(tail - fat_wait):.2f}; step {np.nanmean(nxt - start):.2f} us")
+    for a, b in ((0, 16), (16, 64), (64, 256), (n // 2, n // 2 + 200), (n - 64, n)):
+        seg = slice(a, min(b, n))
+        print(f"    steps {a}-{min(b, n)}: leaf core mean {core_t[seg].mean():.2f} us, step {np.nanmean((nxt - start)[seg]):.2f} us")
     nb = d["nb"]
     first = np.arange(n) % nb == 0
     if first.any():
