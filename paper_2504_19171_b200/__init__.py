@@ -443,11 +443,11 @@ __all__ = [
 
 DTASK_DTYPE = np.dtype({
     "names": ["c_off", "c0_off", "cm_off", "diag_off", "p_off", "ldc", "ldc0", "m0", "n0", "seg_begin", "seg_count",
-              "dep_begin", "sig_begin", "aux0", "aux1", "dep_count", "sig_count", "kind", "mode", "c_store",
+              "dep_begin", "sig_begin", "aux0", "aux1", "poll", "dep_count", "sig_count", "kind", "mode", "c_store",
               "c0_store", "cm_store", "diag_store", "dep2_count", "sig2_count"],
-    "formats": ["<i8"] * 5 + ["<i4"] * 10 + ["<u2"] * 2 + ["u1"] * 8,
-    "offsets": [0, 8, 16, 24, 32, 40, 44, 48, 52, 56, 60, 64, 68, 72, 76, 80, 82, 84, 85, 86, 87, 88, 89, 90, 91],
-    "itemsize": 96,
+    "formats": ["<i8"] * 5 + ["<i4"] * 11 + ["<u2"] * 2 + ["u1"] * 8,
+    "offsets": [0, 8, 16, 24, 32, 40, 44, 48, 52, 56, 60, 64, 68, 72, 76, 80, 88, 90, 92, 93, 94, 95, 96, 97, 98, 99],
+    "itemsize": 104,
 })
 SEG_DTYPE = np.dtype({
     "names": ["a_off", "b_off", "lda", "ldb", "k_lo", "k_hi", "flags", "a_store", "b_store"],

@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <atomic>
 #include <climits>
 #include <cmath>
@@ -157,6 +158,8 @@ struct HostBuf {
 struct DeviceRt {
   int dev = -1;
   cudaStream_t stream = nullptr;
+  cudaStream_t upload = nullptr;  // streamed H2D of the A store, concurrent with the factor sweep
+  int* one = nullptr;             // pinned host 1: the copy engine writes it into upload counters
   bool ready = false;
 };
 static std::mutex g_rt_mu;
@@ -179,6 +182,9 @@ static DeviceRt& runtime(int device) {
     uint64_t thresh = UINT64_MAX;
     CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
     CK(cudaStreamCreateWithFlags(&rt.stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&rt.upload, cudaStreamNonBlocking));
+    CK(cudaMallocHost(reinterpret_cast<void**>(&rt.one), sizeof(int)));
+    *rt.one = 1;
     CK(static_cast<cudaError_t>(configure_kernels()));
     rt.dev = device;
     rt.ready = true;
@@ -196,8 +202,8 @@ struct GraphCache {
     int* sched = nullptr;         // scheduler state: ctl[128], missing[batch x T], slots0, slots1
   };
   std::map<int, Entry> by_batch;
-  Entry& get(int batch, size_t ntasks) {
-    Entry& e = by_batch[batch];
+  Entry& get(int batch, size_t ntasks, bool poll = false) {
+    Entry& e = by_batch[batch * 2 + (poll ? 1 : 0)];
     if (!e.tables) CK(cudaMalloc(reinterpret_cast<void**>(&e.tables), sizeof(BaseTable) * batch));
     if (!e.sched) CK(cudaMalloc(reinterpret_cast<void**>(&e.sched), (128 + 256 + 2 * ntasks * batch) * sizeof(int)));
     return e;
@@ -372,14 +378,19 @@ static void write_trace(DevPlan& P, int batch, unsigned long long* d_trace, cuda
 // Uploads the base tables into the plan-owned buffer, zeroes each matrix's
 // dependency counters and runs the persistent sweep (captured once per batch
 // size into a CUDA graph; its only baked-in pointers are plan-owned).
-static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStream_t s) {
+// pre_launch (streamed upload): issued after the counters are cleared and
+// before the sweep kernel; tasks then poll their A-store column's counter.
+static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStream_t s,
+                     const std::function<void()>* pre_launch = nullptr) {
   std::lock_guard<std::mutex> lk(P.mu);
   const int batch = static_cast<int>(tables.size());
   const size_t nt = P.host.tasks.size();
-  GraphCache::Entry& e = P.graphs.get(batch, nt);
+  const bool poll = pre_launch != nullptr;
+  GraphCache::Entry& e = P.graphs.get(batch, nt, poll);
   CK(cudaMemcpyAsync(e.tables, tables.data(), sizeof(BaseTable) * batch, cudaMemcpyHostToDevice, s));
   for (const BaseTable& t : tables)
     CK(cudaMemsetAsync(t.p[kStoreCounters], 0, static_cast<size_t>(P.host.counters) * sizeof(int), s));
+  if (pre_launch) (*pre_launch)();
   FlowArgs a{};
   a.tasks = P.tasks.p;
   a.segs = P.segs.p;
@@ -398,6 +409,7 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
   a.missing = e.sched + 128 + 256;
   a.chain = P.chain.p;
   a.dedicate = batch <= env_int("TIB_DEDICATE_MAX_BATCH", 4) ? 1 : 0;
+  a.poll_uploads = poll ? 1 : 0;
   a.slots0 = a.missing + nt * batch;
   a.slots1 = a.slots0 + static_cast<size_t>(P.host.q0.count) * batch;
   a.trace = nullptr;
@@ -566,9 +578,10 @@ static double reduce_logdet(const double* parts, int N, int nb) {
 }
 
 // Runs the fused factor sweep for the matrices already resident in their A stores.
-static void factor_sweep(FactorPlan2& P, SweepStores& st, cudaStream_t s, const std::vector<BaseTable>& tables) {
+static void factor_sweep(FactorPlan2& P, SweepStores& st, cudaStream_t s, const std::vector<BaseTable>& tables,
+                         const std::function<void()>* pre_launch = nullptr) {
   CK(cudaMemsetAsync(st.status.p, 0xff, tables.size() * sizeof(unsigned long long), s));
-  run_flow(*P.flow, tables, s);
+  run_flow(*P.flow, tables, s, pre_launch);
 }
 
 static void phase2_sweep(Phase2Plan& P, cudaStream_t s, const std::vector<BaseTable>& tables) {
@@ -613,7 +626,12 @@ static SigmaObj* selected_inverse_matrix(const MatrixObj& m, const Request& req,
   auto p2 = phase2_plan_for(F, sel, device, s);
   SweepStores st;
   alloc_factor_stores(st, *fp, 1, device, s, p2->flow->host.counters, p2->flow->host.scratch_doubles);
-  upload_matrix(m, F, fp->bp, st.A.p, s);
+  // The A store goes up tile column by tile column on the upload stream while
+  // the factor sweep runs (tasks poll each column's counter); only possible
+  // when the host payload already has the device layout (b = bp, no fill-in).
+  const bool stream_up = fp->bp == m.layout.b && F == m.pattern && m.payload.pinned &&
+                         env_int("TIB_STREAM_UPLOAD", 1) != 0 && fp->flow->host.upl >= 0;
+  if (!stream_up) upload_matrix(m, F, fp->bp, st.A.p, s);
   auto* res = new SigmaObj;
   std::unique_ptr<SigmaObj> guard(res);
   res->device = device;
@@ -624,7 +642,30 @@ static SigmaObj* selected_inverse_matrix(const MatrixObj& m, const Request& req,
   res->S = DevBuf(p2->sel.closure.size() * tile, device, s);
   res->var = DevBuf(static_cast<size_t>(m.layout.N) * fp->bp, device, s);
   std::vector<BaseTable> tables{make_table(st.A.p, st.L.p, st.P1.p, res->S.p, res->var.p, st.scratch.p, st.logdet.p, st.status.p, st.ctr(0))};
-  factor_sweep(*fp, st, s, tables);
+  if (stream_up) {
+    cudaEvent_t cleared, uploaded;
+    CK(cudaEventCreateWithFlags(&cleared, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&uploaded, cudaEventDisableTiming));
+    const size_t bb = static_cast<size_t>(fp->bp) * fp->bp;
+    int* upl = reinterpret_cast<int*>(st.ctr(0)) + fp->flow->host.upl;
+    std::function<void()> up = [&]() {
+      CK(cudaEventRecord(cleared, s));
+      CK(cudaStreamWaitEvent(rt.upload, cleared, 0));
+      for (int c = 0; c < m.layout.N; ++c) {
+        const size_t t0 = static_cast<size_t>(F.col_start(c)), t1 = static_cast<size_t>(F.col_start(c + 1));
+        CK(cudaMemcpyAsync(st.A.p + t0 * bb, m.payload.p + t0 * bb, (t1 - t0) * bb * sizeof(double),
+                           cudaMemcpyHostToDevice, rt.upload));
+        CK(cudaMemcpyAsync(upl + c, rt.one, sizeof(int), cudaMemcpyHostToDevice, rt.upload));
+      }
+      CK(cudaEventRecord(uploaded, rt.upload));
+    };
+    factor_sweep(*fp, st, s, tables, &up);
+    CK(cudaStreamWaitEvent(s, uploaded, 0));
+    cudaEventDestroy(cleared);
+    cudaEventDestroy(uploaded);
+  } else {
+    factor_sweep(*fp, st, s, tables);
+  }
   phase2_sweep(*p2, s, tables);
   std::vector<double> parts(fp->flow->host.logdet_doubles);
   CK(cudaMemcpyAsync(parts.data(), st.logdet.p, parts.size() * sizeof(double), cudaMemcpyDeviceToHost, s));

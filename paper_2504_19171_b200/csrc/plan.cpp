@@ -24,6 +24,7 @@ struct Builder {
 
   DTask& add(int q, const std::vector<Dep>& deps, const std::vector<int>& sigs, const std::vector<Dep>& deps2 = {}) {
     DTask t{};
+    t.poll = -1;
     t.dep_begin = static_cast<int>(P.deps.size());
     t.dep_count = static_cast<unsigned short>(deps.size());
     t.dep2_count = static_cast<unsigned char>(deps2.size());
@@ -76,6 +77,7 @@ struct Builder {
         }
       }
       DTask c{};
+      c.poll = -1;
       c.kind = kChainTask;
       c.c_store = c.c0_store = c.cm_store = c.diag_store = kStoreNone;
       c.seg_begin = 0;
@@ -203,7 +205,9 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
   const long cAord = 0, cAfin = cAord + T * NB2, cLblk = cAfin + T, cLfin = cLblk + T * NB2,
              cXblk = cLfin + T, cXfin = cXblk + static_cast<long>(N) * NB2, cTblk = cXfin + N,
              cWfin = cTblk + static_cast<long>(N) * NB2, cXrow = cWfin + T, cArrive = cXrow + static_cast<long>(N) * nb,
-             cSdone = cArrive + static_cast<long>(N) * slots_per_col, cEnd = cSdone + static_cast<long>(N) * nb;
+             cSdone = cArrive + static_cast<long>(N) * slots_per_col, cUpl = cSdone + static_cast<long>(N) * nb,
+             cEnd = cUpl + N;
+  P.upl = cUpl;
   P.counters = cEnd;
   const size_t t_doubles = static_cast<size_t>(N) * bp * bp;
   P.scratch_doubles = t_doubles + static_cast<size_t>(kRing) * slots_per_col * kB * kB;
@@ -579,6 +583,28 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
     if (j - defer_w >= 0) emit_w(j - defer_w);
   }
   for (int j = std::max(0, N - defer_w); j < N; ++j) emit_w(j);
+  // streamed upload: each task polls the upload counter of the latest tile
+  // column of A it reads or writes
+  {
+    const long long tsz2 = static_cast<long long>(bp) * bp;
+    auto col_of = [&](long long off) { return F.tiles()[static_cast<size_t>(off / tsz2)].j; };
+    for (DTask& t : B.all) {
+      int c = -1;
+      if (t.kind == kLeafTask) {
+        c = col_of(t.c_off);
+        if (t.mode & 4) c = std::max(c, col_of(P.segs[static_cast<size_t>(t.seg_begin)].b_off));
+      } else {
+        if (t.c_store == kStoreA) c = std::max(c, col_of(t.c_off));
+        if (t.c0_store == kStoreA) c = std::max(c, col_of(t.c0_off));
+        for (int k = t.seg_begin; k < t.seg_begin + t.seg_count; ++k) {
+          const Seg& g = P.segs[static_cast<size_t>(k)];
+          if (g.a_store == kStoreA) c = std::max(c, col_of(g.a_off));
+          if (g.b_store == kStoreA) c = std::max(c, col_of(g.b_off));
+        }
+      }
+      t.poll = c >= 0 ? static_cast<int>(cUpl + c) : -1;
+    }
+  }
   B.finish(crit_workers, chain);
   return P;
 }

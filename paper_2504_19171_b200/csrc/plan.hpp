@@ -39,6 +39,10 @@ struct DataflowPlan {
   std::vector<int> need, vbase, vidx, init0, init1;
   std::vector<int> wl;
   std::vector<DTask> chain;  // leaf steps of the chain task (kChainTask), in order
+  // streamed upload (factor sweep): counter upl + c is set to 1 by the copy
+  // stream once tile column c of A is resident; every task and chain step that
+  // touches the A store polls the counter of the latest column it touches
+  long upl = -1;
 };
 
 // Fused factorization + phase 1 over the FILLED pattern: per column, the

@@ -86,6 +86,7 @@ struct DTask {
   int seg_begin, seg_count;
   int dep_begin, sig_begin;
   int aux0, aux1;
+  int poll, pad2;  // streamed upload: counter (>= 1 once the A-store column the task touches is uploaded), or -1
   unsigned short dep_count, sig_count;
   unsigned char kind, mode, c_store, c0_store, cm_store, diag_store, dep2_count, sig2_count;
 };

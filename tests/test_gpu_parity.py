@@ -135,13 +135,25 @@ def test_factor_path_and_determinism(tib, orc):
     assert elementwise(diag.diagonal(), ref["diag"]) <= TOL
 
 
-def test_batch_matches_single(tib):
-    ms = [tib.generate(5000, 500, 50, 1.0, seed=1000 + k, tile_size=128) for k in range(3)]
+@pytest.mark.parametrize("count", [3, 6])  # 6 > TIB_DEDICATE_MAX_BATCH: chains share their SMs
+def test_batch_matches_single(tib, count):
+    ms = [tib.generate(5000, 500, 50, 1.0, seed=1000 + k, tile_size=128) for k in range(count)]
     logdet, diag = tib.selected_inverse_batch(ms)
     for k, m in enumerate(ms):
         res = tib.selected_inverse(m, "pattern")
         assert logdet[k] == res.logdet()
         assert np.array_equal(diag[k], res.diagonal())
+
+
+def test_streamed_upload_is_bitwise_identical(tib, monkeypatch):
+    """The public path streams A up column by column under the factor sweep
+    (tasks poll per-column upload counters); the result must not depend on it."""
+    m = tib.generate(6000, 700, 60, 1.0, seed=23, tile_size=256)
+    streamed = tib.selected_inverse(m, "pattern")
+    monkeypatch.setenv("TIB_STREAM_UPLOAD", "0")
+    upfront = tib.selected_inverse(m, "pattern")
+    assert streamed.checksum == upfront.checksum
+    assert streamed.logdet() == upfront.logdet()
 
 
 @pytest.mark.parametrize("cfg", [
