@@ -64,7 +64,7 @@ int main() {
   cudaMemcpy(dP, p.data(), 32768, cudaMemcpyHostToDevice);
   cudaMemset(st, 0xff, 8);
   cudaFuncSetAttribute(chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFlowSmemBytes);
-  for (int mode : {1, 1, 1}) {
+  for (int mode : {0, 1, 2, 0, 1, 2}) {
     chain_kernel<<<1, 128, kFlowSmemBytes>>>(dA, dP, dA, dL, dX, dPo, st, dld, cyc, 50, mode);
     long long c[2];
     cudaMemcpy(c, cyc, 16, cudaMemcpyDeviceToHost);

@@ -25,6 +25,29 @@ __global__ void chol_kernel(const double* A, double* out, long long* cyc, int re
   for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) out[i] = SX[(i / 32) * kLs + i % 32];
 }
 
+// warp-specialised chol32 (chol32_l on warp 0, chol32_x on warp 1)
+__global__ void split_kernel(const double* A, double* out, long long* cyc, int reps) {
+  extern __shared__ __align__(16) double smem[];
+  double* SA = smem;
+  double* SX = smem + kLeaf * kLs;
+  double* vec = SX + kLeaf * kLs;
+  for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) SA[(i / 32) * kLs + i % 32] = A[i];
+  __syncthreads();
+  long long t0 = clock64();
+  volatile int* flag = reinterpret_cast<volatile int*>(vec + 7 * kL2);
+  for (int r = 0; r < reps; ++r) {
+    if (threadIdx.x == 0) *flag = 0;
+    __syncthreads();
+    if (threadIdx.x < 32) chol32_l<true>(SA, SX + kL2, vec + 128, vec + 288, vec + 192, flag);
+    else if (threadIdx.x < 64) chol32_x(SX, SX + kL2, vec + 192, flag);
+    __syncthreads();
+    for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) SA[(i / 32) * kLs + i % 32] = A[i];
+    __syncthreads();
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[0] = (t1 - t0) / reps;
+}
+
 __global__ void chol2_kernel(const double* A, long long* cyc, int mode) {
   extern __shared__ __align__(16) double smem[];
   double* SA = smem;
@@ -126,6 +149,12 @@ int main() {
     chol_kernel<true, false, false><<<1, 32, kFlowSmemBytes>>>(dA32, dout, cyc, 20);
     cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
     printf("{\"chol32_chain_only_cycles\": %lld}\n", c);
+  }
+  cudaFuncSetAttribute(split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFlowSmemBytes);
+  for (int it = 0; it < 2; ++it) {
+    split_kernel<<<1, 128, kFlowSmemBytes>>>(dA32, dout, cyc, 20);
+    cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("{\"chol32_split_cycles_incl_reload\": %lld}\n", c);
   }
   cudaFuncSetAttribute(chol2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFlowSmemBytes);
   for (int mode : {0, 1, 0, 1}) {
