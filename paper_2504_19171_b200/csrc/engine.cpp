@@ -249,7 +249,13 @@ static int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e && *e ? std::atoi(e) : dflt;
 }
-static int crit_workers() { return env_int("TIB_CRIT_WORKERS", 12); }
+// CTAs reserved for the critical queue: the factor sweep's q0 (the chain's
+// helpers) is heavy and latency-sensitive, phase 2's (diagonal parts) is light
+static int crit_workers(bool factor) {
+  const int all = env_int("TIB_CRIT_WORKERS", 0);
+  if (all > 0) return all;
+  return factor ? env_int("TIB_CRIT_WORKERS_FACTOR", 40) : env_int("TIB_CRIT_WORKERS_P2", 12);
+}
 
 static std::shared_ptr<DevPlan> upload_plan(DataflowPlan&& host, int device, cudaStream_t s) {
   auto d = std::make_shared<DevPlan>();
@@ -297,7 +303,7 @@ static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int 
   auto plan = std::make_shared<FactorPlan2>();
   plan->sym = symbolic_cholesky(pattern);
   plan->L = plan->sym.filled.layout();
-  plan->flow = upload_plan(build_factor_dataflow(plan->sym.filled, crit_workers(), env_int("TIB_DEFER_W", 2),
+  plan->flow = upload_plan(build_factor_dataflow(plan->sym.filled, crit_workers(true), env_int("TIB_DEFER_W", 2),
                                                   env_int("TIB_FAT_LEAF", 0) != 0, env_int("TIB_CHAIN", 1) != 0,
                                                   env_int("TIB_CHAIN", 1) != 0 && env_int("TIB_BOUNDARY", 1) != 0),
                            device, s);
@@ -319,7 +325,7 @@ static std::shared_ptr<Phase2Plan> phase2_plan_for(const Pattern& F, const Closu
   }
   auto plan = std::make_shared<Phase2Plan>();
   plan->sel = sel;
-  plan->flow = upload_plan(build_phase2_dataflow(F, plan->sel, crit_workers()), device, s);
+  plan->flow = upload_plan(build_phase2_dataflow(F, plan->sel, crit_workers(false)), device, s);
   plan->bp = plan->flow->host.bp;
   plan->nb = plan->flow->host.nb;
   std::lock_guard<std::mutex> lk(g_plan_mu);

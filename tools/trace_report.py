@@ -96,6 +96,11 @@ def chain_report(d, t0):
         seg = slice(a, min(b, n))
         print(f"    steps {a}-{min(b, n)}: leaf core mean {core_t[seg].mean():.2f} us, step {np.nanmean((nxt - start)[seg]):.2f} us")
     nb = d["nb"]
+    pos = np.arange(n) % nb
+    for k in range(nb):
+        m = pos == k
+        print(f"    block {k} of the tile: leaf core {core_t[m].mean():.2f} us, fat wait {fat_wait[m].mean():.2f}, "
+              f"rest to next step {np.nanmean((nxt - core - fat_wait)[m]):.2f}, step {np.nanmean((nxt - start)[m]):.2f}")
     first = np.arange(n) % nb == 0
     if first.any():
         print(f"    tile-first steps: dep wait mean {dep_wait[first].mean():.2f} us (total {dep_wait[first].sum() / 1e3:.1f} ms); "
