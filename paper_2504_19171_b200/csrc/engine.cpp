@@ -377,6 +377,7 @@ static void write_trace(DevPlan& P, int batch, unsigned long long* d_trace, cuda
   std::fwrite(P.host.sigs.data(), sizeof(int), P.host.sigs.size(), f);
   std::fwrite(P.host.segs.data(), sizeof(Seg), P.host.segs.size(), f);
   std::fwrite(P.host.slot_tiles.data(), sizeof(Coord), P.host.slot_tiles.size(), f);
+  std::fwrite(P.host.chain.data(), sizeof(DTask), P.host.chain.size(), f);
   std::fwrite(h.data(), 8, n, f);
   std::fclose(f);
 }

@@ -196,16 +196,28 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
   // tile-boundary trick (boundary && nb >= 2): per row p of the first tile,
   // S_p = sum_{k < nb-1} A(k0, j)[p, k] T(nb-1, k)^T split over parts of <= 128,
   // plus the reduced S_p block itself
+  // With the boundary trick every block column q >= 1 of the first tile's panel
+  // is formed the same way: S^q_p = sum_{k<q} A(k0, j)[p, k] T(q, k)^T (reduced
+  // while leaf q runs), L(k0, j)[p, q] = (A(k0, j)[p, q] - S^q_p) X_q^T -- no
+  // row of X_j on the path.
   const bool bnd = boundary && nb >= 2;
-  const int s_parts = bnd ? (nb - 1 + 1) / 2 : 0;
-  const int s_slots = bnd ? nb * (s_parts > 1 ? s_parts : 0) + nb : 0;
+  auto s_parts = [&](int q) { return (q + 1) / 2; };  // K = 64 q, parts of <= 128
+  std::vector<int> sq_part_base(static_cast<size_t>(nb) + 1, 0), sq_out_base(static_cast<size_t>(nb) + 1, 0);
+  int s_slots = 0;
+  if (bnd)
+    for (int q = 1; q < nb; ++q) {
+      sq_part_base[static_cast<size_t>(q)] = s_slots;
+      s_slots += s_parts(q) > 1 ? nb * s_parts(q) : 0;
+      sq_out_base[static_cast<size_t>(q)] = s_slots;
+      s_slots += nb;
+    }
   const int slots_per_col = 2 * panel_slots + 2 * upd_slots + s_slots;
   constexpr int kRing = 4;  // columns of partial slots in flight (see the reuse argument below)
   // counter spaces
   const long cAord = 0, cAfin = cAord + T * NB2, cLblk = cAfin + T, cLfin = cLblk + T * NB2,
              cXblk = cLfin + T, cXfin = cXblk + static_cast<long>(N) * NB2, cTblk = cXfin + N,
              cWfin = cTblk + static_cast<long>(N) * NB2, cXrow = cWfin + T, cArrive = cXrow + static_cast<long>(N) * nb,
-             cSdone = cArrive + static_cast<long>(N) * slots_per_col, cUpl = cSdone + static_cast<long>(N) * nb,
+             cSdone = cArrive + static_cast<long>(N) * slots_per_col, cUpl = cSdone + static_cast<long>(N) * NB2,
              cEnd = cUpl + N;
   P.upl = cUpl;
   P.counters = cEnd;
@@ -221,7 +233,7 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
   auto tcnt = [&](int j, int p, int q) { return static_cast<int>(cTblk + static_cast<long>(j) * NB2 + p * nb + q); };
   auto wfin = [&](long s) { return static_cast<int>(cWfin + s); };
   auto xrowc = [&](int j, int q) { return static_cast<int>(cXrow + static_cast<long>(j) * nb + q); };
-  auto sdone = [&](int j, int p) { return static_cast<int>(cSdone + static_cast<long>(j) * nb + p); };
+  auto sdone = [&](int j, int q, int p) { return static_cast<int>(cSdone + static_cast<long>(j) * NB2 + q * nb + p); };
   const int xdone = nb * (nb + 1) / 2;
   const long long tsz = static_cast<long long>(bp) * bp;
 
@@ -268,9 +280,10 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
     if (tail0) u00 = ord[static_cast<size_t>(ts00)]++;
     if (tail1) u10 = ord[static_cast<size_t>(F.slot(krows[1], krows[0]))]++;
     const bool bnd_col = bnd && tail0;
-    auto s_off = [&](int p) {  // reduced S_p block of this column (ring slot)
+    auto s_off = [&](int q, int p) {  // reduced S^q_p block of this column (ring slot)
       return static_cast<long long>(t_doubles) +
-             (static_cast<long long>(j % kRing) * slots_per_col + 2 * panel_slots + 2 * upd_slots + nb * (s_parts > 1 ? s_parts : 0) + p) *
+             (static_cast<long long>(j % kRing) * slots_per_col + 2 * panel_slots + 2 * upd_slots +
+              sq_out_base[static_cast<size_t>(q)] + p) *
                  kB * kB;
     };
     // ---- diagonal-tile chain (queue 0): blocked POTRF + TRTRI of tile (j, j)
@@ -293,7 +306,7 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
         sg.push_back(lfin(ds));
         sg.push_back(aord(ds, kk + 1, kk + 1));
       } else if (bleaf) {
-        d2.push_back({sdone(j, 0), 1});
+        d2.push_back({sdone(j, nb - 1, 0), 1});
         d2.push_back({afin(sk0), Uk0 * NB2});
         d2.push_back({aord(ts00, 0, 0), u00 + 1});
         sg.push_back(lblk(sk0, 0, nb - 1));
@@ -308,7 +321,7 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
         t.p_off = blk_off(sk0, bp, 0, nb - 1);  // P in the A store; L(k0, j)[0, nb-1] at the same offset in L
         Seg sgx{};
         sgx.a_store = kStoreScratch;
-        sgx.a_off = s_off(0);                    // S_0
+        sgx.a_off = s_off(nb - 1, 0);            // S^{nb-1}_0
         sgx.b_store = kStoreA;
         sgx.b_off = blk_off(ts00, bp, 0, 0);     // next diagonal block
         sgx.lda = kB;  // S_0 is a 64x64 block
@@ -448,47 +461,50 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
       return kk == nb - 1 ? 0 : -1;
     };
 
-    // S_p = sum_{k < nb-1} A(k0, j)[p, k] T(nb-1, k)^T (split-K over parts of <= 128);
-    // ready once row nb-1 of T is accumulated, i.e. during the chain's last leaf
-    auto s_tasks = [&]() {
-      const int K = (nb - 1) * kB;
+    // S^q_p = sum_{l < q} L(k0, j)[p, l] L(j, j)[q, l]^T (= sum_{k<q} A(k0, j)[p, k]
+    // T(q, k)^T, the right-looking form: no row of X_j needed), split-K over
+    // parts of <= 128 in l; each part runs once its panel blocks exist
+    auto s_tasks = [&](int q) {
+      const int K = q * kB, sp = s_parts(q);
       for (int p = 0; p < nb; ++p) {
-        for (int r = 0; r < s_parts; ++r) {
-          const int klo = s_parts > 1 ? r * 2 * kB : 0, khi = s_parts > 1 ? std::min(K, (r + 1) * 2 * kB) : K;
-          std::vector<Dep> d{{afin(sk0), Uk0 * NB2}};
-          for (int k = klo / kB; k < khi / kB; ++k) d.push_back({tcnt(j, nb - 1, k), nb - 1 - k});
-          DTask& t = B.add(0, d, {sdone(j, p)});
-          t.kind = s_parts > 1 ? kSplitTask : kGemmTask;
+        for (int r = 0; r < sp; ++r) {
+          const int klo = sp > 1 ? r * 2 * kB : 0, khi = sp > 1 ? std::min(K, (r + 1) * 2 * kB) : K;
+          std::vector<Dep> d;
+          for (int l = klo / kB; l < khi / kB; ++l) {
+            d.push_back({lblk(sk0, p, l), 1});
+            d.push_back({lblk(ds, q, l), 1});
+          }
+          DTask& t = B.add(0, d, {sdone(j, q, p)});
+          t.kind = sp > 1 ? kSplitTask : kGemmTask;
           t.c_store = kStoreScratch;
-          t.c_off = s_off(p);
+          t.c_off = s_off(q, p);
           t.ldc = kB;
-          if (s_parts > 1) {
-            const int slot = 2 * panel_slots + 2 * upd_slots + p * s_parts;
+          if (sp > 1) {
+            const int slot = 2 * panel_slots + 2 * upd_slots + sq_part_base[static_cast<size_t>(q)] + p * sp;
             t.p_off = static_cast<long long>(t_doubles) +
                       (static_cast<long long>(j % kRing) * slots_per_col + slot) * kB * kB;
             t.aux0 = static_cast<int>(cArrive + static_cast<long>(j) * slots_per_col + slot);
-            t.aux1 = (r << 8) | s_parts;
+            t.aux1 = (r << 8) | sp;
           }
-          for (int k = klo / kB; k < khi / kB; ++k)
-            B.seg(t, kStoreA, blk_off(sk0, bp, p, k), kStoreScratch,
-                  tsz * j + static_cast<long long>(nb - 1) * kB * bp + k * kB, 0, kB, kTransB);
+          for (int l = klo / kB; l < khi / kB; ++l)
+            B.seg(t, kStoreL, blk_off(sk0, bp, p, l), kStoreL, blk_off(ds, bp, q, l), 0, kB, kTransB);
         }
       }
     };
-    // L(k0, j)[p, nb-1] = (A(k0, j)[p, nb-1] - S_p) X_{nb-1}^T for rows p >= 1 (row 0: the chain)
-    auto last_panel = [&]() {
-      const long long xd = blk_off(ds, bp, nb - 1, nb - 1);
-      for (int p = 1; p < nb; ++p) {
-        DTask& t = B.add(0, {{xblk(j, nb - 1, nb - 1), 1}, {sdone(j, p), 1}, {afin(sk0), Uk0 * NB2}},
-                         {lblk(sk0, p, nb - 1), lfin(sk0)});
+    // L(k0, j)[p, q] = (A(k0, j)[p, q] - S^q_p) X_q^T (for q = nb-1, row 0 is the chain's)
+    auto s_panel = [&](int q) {
+      const long long xd = blk_off(ds, bp, q, q);
+      for (int p = q == nb - 1 ? 1 : 0; p < nb; ++p) {
+        DTask& t = B.add(0, {{xblk(j, q, q), 1}, {sdone(j, q, p), 1}, {afin(sk0), Uk0 * NB2}},
+                         {lblk(sk0, p, q), lfin(sk0)});
         t.kind = kGemmTask;
         t.c_store = kStoreL;
-        t.c_off = blk_off(sk0, bp, p, nb - 1);
-        B.seg(t, kStoreA, blk_off(sk0, bp, p, nb - 1), kStoreP1, xd, 0, kB, kTransB);
+        t.c_off = blk_off(sk0, bp, p, q);
+        B.seg(t, kStoreA, blk_off(sk0, bp, p, q), kStoreP1, xd, 0, kB, kTransB);
         Seg& sg = P.segs.emplace_back();
         sg = Seg{};
         sg.a_store = kStoreScratch;
-        sg.a_off = s_off(p);
+        sg.a_off = s_off(q, p);
         sg.lda = kB;
         sg.b_store = kStoreP1;
         sg.b_off = xd;
@@ -519,8 +535,8 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
         const int r = upd_part_at(kk);
         if (r >= 0) update_split(0, 0, r, u00, 0, 2 * panel_slots);
       } else if (tail0) {
-        if (kk < nb - 1) panel_prog(0, kk, 0, 0);
-        else last_panel();
+        if (kk == 0) panel_prog(0, 0, 0, 0);
+        else s_panel(kk);
         const int r = upd_part_at(kk);
         if (r >= 0) update_split(0, 0, r, u00, 0, 2 * panel_slots, 1);
         // block (0, 0): its clipped last part goes out one step early
@@ -532,7 +548,7 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
         } else if (kk == nb - 2) {
           update_split(0, 0, 0, u00, 0, 2 * panel_slots, 2);
         }
-        if (kk == nb - 2) s_tasks();
+        if (kk + 1 < nb) s_tasks(kk + 1);
       }
     }
     if (tail1) {

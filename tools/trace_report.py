@@ -37,10 +37,11 @@ def load(path):
         sigs = np.frombuffer(f.read(4 * nsig), np.int32)
         segs = np.frombuffer(f.read(32 * nseg), SEG)
         tiles = np.frombuffer(f.read(8 * ntiles), np.int32).reshape(-1, 2)
+        chain_tasks = np.frombuffer(f.read(DTASK.itemsize * nchain), DTASK)
         rec = np.frombuffer(f.read(), np.uint64).reshape(-1, 4)
     chain = rec[ntask * batch:]
     rec = rec[:ntask * batch]
-    return dict(chain=chain,ntask=ntask, batch=batch, nq0=nq0, nb=nb, tasks=tasks, deps=deps, sigs=sigs, segs=segs, rec=rec,
+    return dict(chain=chain, chain_tasks=chain_tasks,ntask=ntask, batch=batch, nq0=nq0, nb=nb, tasks=tasks, deps=deps, sigs=sigs, segs=segs, rec=rec,
                 tiles=tiles, bp=bp)
 
 
@@ -105,6 +106,33 @@ def chain_report(d, t0):
     if first.any():
         print(f"    tile-first steps: dep wait mean {dep_wait[first].mean():.2f} us (total {dep_wait[first].sum() / 1e3:.1f} ms); "
               f"other steps dep wait total {dep_wait[~first].sum() / 1e3:.1f} ms, fat waits total {fat_wait.sum() / 1e3:.1f} ms")
+
+
+def chain_deps_report(d, events, t0):
+    """For the chain's boundary steps (mode 4): when each second-phase dependency
+    was satisfied, relative to the end of the step's first phase."""
+    ch = d["chain"].astype(np.float64) / 1e3
+    if len(ch) == 0:
+        return
+    tasks_chain = d.get("chain_tasks")
+    if tasks_chain is None:
+        return
+    deps = d["deps"]
+    lat = {}
+    nb = d["nb"]
+    for si, st in enumerate(tasks_chain):
+        if not (st["mode"] & 4 or si % nb == 0) or ch[si, 2] <= 0:
+            continue
+        core_end = ch[si, 2] - t0
+        for k in range(st["dep_begin"] + st["dep_count"], st["dep_begin"] + st["dep_count"] + st["dep2_count"]):
+            dp = deps[k]
+            ev = events.get((int(dp["counter"]), 0), [])
+            if dp["value"] > 0 and len(ev) >= dp["value"]:
+                key = ("boundary" if st["mode"] & 4 else "block0", k - st["dep_begin"] - st["dep_count"])
+                lat.setdefault(key, []).append(ev[dp["value"] - 1][0] - core_end)
+    for k, v in sorted(lat.items()):
+        v = np.array(v)
+        print(f"    {k[0]} dep2[{k[1]}] satisfied {v.mean():+.1f} us after the leaf (p50 {np.median(v):+.1f}, max {v.max():+.1f})")
 
 
 def report(path):
@@ -179,6 +207,7 @@ def report(path):
         if len(w):
             print(f"  {name} queue wait (claim - pushed): mean {w.mean():.2f} us, p50 {np.median(w):.2f}, p90 "
                   f"{np.percentile(w, 90):.2f}, max {w.max():.1f}")
+    chain_deps_report(d, events, t0)
     r = int(np.argmax(done))
     path_seq = []
     path_exec = collections.Counter()
