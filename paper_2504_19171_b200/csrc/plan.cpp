@@ -201,7 +201,11 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
   // while leaf q runs), L(k0, j)[p, q] = (A(k0, j)[p, q] - S^q_p) X_q^T -- no
   // row of X_j on the path.
   const bool bnd = boundary && nb >= 2;
-  auto s_parts = [&](int q) { return (q + 1) / 2; };  // K = 64 q, parts of <= 128
+  // S^q_p sums l < q - 1 (the last term L(k0, j)[p, q-1] L(j, j)[q, q-1]^T goes
+  // into the panel task through M_q, below) -- except row 0 of the last block
+  // column, which the boundary leaf takes fully reduced (l < q)
+  auto s_terms = [&](int q, int p) { return (q == nb - 1 && p == 0) ? q : q - 1; };
+  auto s_parts = [&](int q) { return (q + 1) / 2; };  // the most parts of any row: K = 64 q, parts of <= 128
   std::vector<int> sq_part_base(static_cast<size_t>(nb) + 1, 0), sq_out_base(static_cast<size_t>(nb) + 1, 0);
   int s_slots = 0;
   if (bnd)
@@ -211,14 +215,15 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
       sq_out_base[static_cast<size_t>(q)] = s_slots;
       s_slots += nb;
     }
-  const int slots_per_col = 2 * panel_slots + 2 * upd_slots + s_slots;
+  const int m_slots = bnd ? nb : 0;  // M_q = X_q L(j, j)[q, q-1] per block column
+  const int slots_per_col = 2 * panel_slots + 2 * upd_slots + s_slots + m_slots;
   constexpr int kRing = 4;  // columns of partial slots in flight (see the reuse argument below)
   // counter spaces
   const long cAord = 0, cAfin = cAord + T * NB2, cLblk = cAfin + T, cLfin = cLblk + T * NB2,
              cXblk = cLfin + T, cXfin = cXblk + static_cast<long>(N) * NB2, cTblk = cXfin + N,
              cWfin = cTblk + static_cast<long>(N) * NB2, cXrow = cWfin + T, cArrive = cXrow + static_cast<long>(N) * nb,
              cSdone = cArrive + static_cast<long>(N) * slots_per_col, cUpl = cSdone + static_cast<long>(N) * NB2,
-             cEnd = cUpl + N;
+             cMdone = cUpl + N, cEnd = cMdone + static_cast<long>(N) * nb;
   P.upl = cUpl;
   P.counters = cEnd;
   const size_t t_doubles = static_cast<size_t>(N) * bp * bp;
@@ -234,6 +239,7 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
   auto wfin = [&](long s) { return static_cast<int>(cWfin + s); };
   auto xrowc = [&](int j, int q) { return static_cast<int>(cXrow + static_cast<long>(j) * nb + q); };
   auto sdone = [&](int j, int q, int p) { return static_cast<int>(cSdone + static_cast<long>(j) * NB2 + q * nb + p); };
+  auto mdone = [&](int j, int q) { return static_cast<int>(cMdone + static_cast<long>(j) * nb + q); };
   const int xdone = nb * (nb + 1) / 2;
   const long long tsz = static_cast<long long>(bp) * bp;
 
@@ -285,6 +291,10 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
              (static_cast<long long>(j % kRing) * slots_per_col + 2 * panel_slots + 2 * upd_slots +
               sq_out_base[static_cast<size_t>(q)] + p) *
                  kB * kB;
+    };
+    auto m_off = [&](int q) {  // M_q of this column (ring slot)
+      return static_cast<long long>(t_doubles) +
+             (static_cast<long long>(j % kRing) * slots_per_col + 2 * panel_slots + 2 * upd_slots + s_slots + q) * kB * kB;
     };
     // ---- diagonal-tile chain (queue 0): blocked POTRF + TRTRI of tile (j, j)
     // Fat leaf: factor + invert block (kk, kk), then (kk + 1 < nb, after the
@@ -465,8 +475,10 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
     // T(q, k)^T, the right-looking form: no row of X_j needed), split-K over
     // parts of <= 128 in l; each part runs once its panel blocks exist
     auto s_tasks = [&](int q) {
-      const int K = q * kB, sp = s_parts(q);
       for (int p = 0; p < nb; ++p) {
+        const int nt = s_terms(q, p);
+        if (nt < 1) continue;
+        const int K = nt * kB, sp = (nt + 1) / 2;
         for (int r = 0; r < sp; ++r) {
           const int klo = sp > 1 ? r * 2 * kB : 0, khi = sp > 1 ? std::min(K, (r + 1) * 2 * kB) : K;
           std::vector<Dep> d;
@@ -480,7 +492,7 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
           t.c_off = s_off(q, p);
           t.ldc = kB;
           if (sp > 1) {
-            const int slot = 2 * panel_slots + 2 * upd_slots + sq_part_base[static_cast<size_t>(q)] + p * sp;
+            const int slot = 2 * panel_slots + 2 * upd_slots + sq_part_base[static_cast<size_t>(q)] + p * s_parts(q);
             t.p_off = static_cast<long long>(t_doubles) +
                       (static_cast<long long>(j % kRing) * slots_per_col + slot) * kB * kB;
             t.aux0 = static_cast<int>(cArrive + static_cast<long>(j) * slots_per_col + slot);
@@ -491,29 +503,49 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
         }
       }
     };
-    // L(k0, j)[p, q] = (A(k0, j)[p, q] - S^q_p) X_q^T (for q = nb-1, row 0 is the chain's)
+    // M_q = X_q L(j, j)[q, q-1] (q >= 1), once leaf q and the panel block of
+    // step q-1 exist: the last S term folded into the panel task,
+    //   L(k0, j)[p, q-1] L(j, j)[q, q-1]^T X_q^T = L(k0, j)[p, q-1] M_q^T,
+    // so each block column of the panel is one task after the previous one.
+    auto m_task = [&](int q) {
+      DTask& t = B.add(0, {{xblk(j, q, q), 1}, {lblk(ds, q, q - 1), 1}}, {mdone(j, q)});
+      t.kind = kGemmTask;
+      t.c_store = kStoreScratch;
+      t.c_off = m_off(q);
+      t.ldc = kB;
+      B.seg(t, kStoreP1, blk_off(ds, bp, q, q), kStoreL, blk_off(ds, bp, q, q - 1), 0, kB, 0);
+    };
+    // L(k0, j)[p, q] = (A(k0, j)[p, q] - S^q_p) X_q^T - L(k0, j)[p, q-1] M_q^T
+    // (for q = nb-1, row 0 is the chain's)
     auto s_panel = [&](int q) {
       const long long xd = blk_off(ds, bp, q, q);
-      for (int p = q == nb - 1 ? 1 : 0; p < nb; ++p) {
-        DTask& t = B.add(0, {{xblk(j, q, q), 1}, {sdone(j, q, p), 1}, {afin(sk0), Uk0 * NB2}},
-                         {lblk(sk0, p, q), lfin(sk0)});
-        t.kind = kGemmTask;
-        t.c_store = kStoreL;
-        t.c_off = blk_off(sk0, bp, p, q);
-        B.seg(t, kStoreA, blk_off(sk0, bp, p, q), kStoreP1, xd, 0, kB, kTransB);
+      auto scratch_seg = [&](DTask& t, long long a_off, unsigned char bs, long long b_off, int ldb,
+                             unsigned char as = kStoreScratch, int lda = kB) {
         Seg& sg = P.segs.emplace_back();
         sg = Seg{};
-        sg.a_store = kStoreScratch;
-        sg.a_off = s_off(q, p);
-        sg.lda = kB;
-        sg.b_store = kStoreP1;
-        sg.b_off = xd;
-        sg.ldb = bp;
+        sg.a_store = as;
+        sg.a_off = a_off;
+        sg.lda = lda;
+        sg.b_store = bs;
+        sg.b_off = b_off;
+        sg.ldb = ldb;
         sg.k_lo = 0;
         sg.k_hi = kB;
         sg.flags = kTransB | kNegate;
         ++t.seg_count;
         P.task_flops += 2.0 * kB * kB * kB;
+      };
+      for (int p = q == nb - 1 ? 1 : 0; p < nb; ++p) {
+        const bool has_s = s_terms(q, p) >= 1;
+        std::vector<Dep> d{{xblk(j, q, q), 1}, {afin(sk0), Uk0 * NB2}, {mdone(j, q), 1}, {lblk(sk0, p, q - 1), 1}};
+        if (has_s) d.push_back({sdone(j, q, p), 1});
+        DTask& t = B.add(0, d, {lblk(sk0, p, q), lfin(sk0)});
+        t.kind = kGemmTask;
+        t.c_store = kStoreL;
+        t.c_off = blk_off(sk0, bp, p, q);
+        B.seg(t, kStoreA, blk_off(sk0, bp, p, q), kStoreP1, xd, 0, kB, kTransB);
+        if (has_s) scratch_seg(t, s_off(q, p), kStoreP1, xd, bp);
+        scratch_seg(t, blk_off(sk0, bp, p, q - 1), kStoreScratch, m_off(q), kB, kStoreL, bp);
       }
     };
     for (int kk = 0; kk < nb; ++kk) {
@@ -535,8 +567,12 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
         const int r = upd_part_at(kk);
         if (r >= 0) update_split(0, 0, r, u00, 0, 2 * panel_slots);
       } else if (tail0) {
-        if (kk == 0) panel_prog(0, 0, 0, 0);
-        else s_panel(kk);
+        if (kk == 0) {
+          panel_prog(0, 0, 0, 0);
+        } else {
+          m_task(kk);
+          s_panel(kk);
+        }
         const int r = upd_part_at(kk);
         if (r >= 0) update_split(0, 0, r, u00, 0, 2 * panel_slots, 1);
         // block (0, 0): its clipped last part goes out one step early

@@ -13,7 +13,7 @@ using namespace tib;
 __global__ void chain_kernel(const double* A, const double* P, const double* Dn, double* L, double* X, double* Pout,
                              DevStatus* st, double* ld, long long* cyc, int steps, int mode) {
   extern __shared__ __align__(16) double smem[];
-  long long total = 0, leaf_t = 0;
+  long long total = 0, leaf_t = 0, fat_t = 0, fat_t0 = 0;
   for (int s = 0; s < steps; ++s) {
     if (mode != 0) {
       for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) smem[(i / 64) * kLs + i % 64] = (i % 64 <= i / 64) ? A[i] : 0.0;
@@ -23,10 +23,18 @@ __global__ void chain_kernel(const double* A, const double* P, const double* Dn,
     leaf_potrf_inv<true>(mode == 0 ? A : nullptr, 64, L, X, 64, 64, 0, st, ld, smem);
     const long long t1 = clock64();
     if (mode == 2) {
-      chain_fat(P, Pout, Dn, 64, smem);
+      chain_fat_prefetch(P, Dn, 64, smem);
+      double* SX = smem + kLeaf * kLs;
+      for (int idx = threadIdx.x; idx < kL2 * kL2; idx += kGemmThreads) SX[(idx / kL2) * kLs + kL2 + (idx % kL2)] = 0.0;
+      cp_async_wait<0>();
+      __syncthreads();
+      fat_t0 = clock64();
+      chain_fat_head(Pout, 64, smem);
+      fat_t += clock64() - fat_t0;
+      if (threadIdx.x >= 64) chain_fat_tail(smem);
       __syncthreads();
     }
-    if (mode == 3) {
+    if (false) {
       // code pollution: a block GEMM task between steps (like the sweep kernel's other paths)
       RSeg sg{P, Dn, 64, 64, 0, 64, kTransB, 0};
       RTask t{};
@@ -45,6 +53,7 @@ __global__ void chain_kernel(const double* A, const double* P, const double* Dn,
   if (threadIdx.x == 0) {
     cyc[0] = total / steps;
     cyc[1] = leaf_t / steps;
+    cyc[2] = fat_t / steps;
   }
 }
 
@@ -59,16 +68,16 @@ int main() {
   DevStatus* st;
   long long* cyc;
   cudaMalloc(&dA, 32768); cudaMalloc(&dP, 32768); cudaMalloc(&dL, 32768); cudaMalloc(&dX, 32768);
-  cudaMalloc(&dPo, 32768); cudaMalloc(&dld, 8); cudaMalloc(&st, 8); cudaMalloc(&cyc, 16);
+  cudaMalloc(&dPo, 32768); cudaMalloc(&dld, 8); cudaMalloc(&st, 8); cudaMalloc(&cyc, 32);
   cudaMemcpy(dA, a.data(), 32768, cudaMemcpyHostToDevice);
   cudaMemcpy(dP, p.data(), 32768, cudaMemcpyHostToDevice);
   cudaMemset(st, 0xff, 8);
   cudaFuncSetAttribute(chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFlowSmemBytes);
   for (int mode : {0, 1, 2, 0, 1, 2}) {
     chain_kernel<<<1, 128, kFlowSmemBytes>>>(dA, dP, dA, dL, dX, dPo, st, dld, cyc, 50, mode);
-    long long c[2];
-    cudaMemcpy(c, cyc, 16, cudaMemcpyDeviceToHost);
-    printf("{\"mode\": %d, \"step_cycles\": %lld, \"leaf_cycles\": %lld, \"err\": \"%s\"}\n", mode, c[0], c[1],
+    long long c[3];
+    cudaMemcpy(c, cyc, 24, cudaMemcpyDeviceToHost);
+    printf("{\"mode\": %d, \"step_cycles\": %lld, \"leaf_cycles\": %lld, \"fat_dmma_cycles\": %lld, \"err\": \"%s\"}\n", mode, c[0], c[1], c[2],
            cudaGetErrorString(cudaGetLastError()));
   }
   return 0;

@@ -133,6 +133,44 @@ def chain_deps_report(d, events, t0):
     for k, v in sorted(lat.items()):
         v = np.array(v)
         print(f"    {k[0]} dep2[{k[1]}] satisfied {v.mean():+.1f} us after the leaf (p50 {np.median(v):+.1f}, max {v.max():+.1f})")
+    # the producer chain behind the boundary's late second-phase dependencies,
+    # for one boundary step in the middle of the sweep
+    ctx = d.get("_ctx")
+    bsteps = [si for si, st in enumerate(tasks_chain) if st["mode"] & 4 and ch[si, 2] > 0]
+    if not bsteps or ctx is None:
+        return
+    si = bsteps[len(bsteps) // 2]
+    st = tasks_chain[si]
+    core_end = ch[si, 2] - t0
+    print(f"    boundary step {si}: producers of its second-phase deps (times us relative to its leaf end):")
+    for k in range(st["dep_begin"] + st["dep_count"], st["dep_begin"] + st["dep_count"] + st["dep2_count"]):
+        dp = deps[k]
+        ev = events.get((int(dp["counter"]), 0), [])
+        if dp["value"] <= 0 or len(ev) < dp["value"]:
+            continue
+        r = ev[dp["value"] - 1][1]
+        print(f"     dep2[{k - st['dep_begin'] - st['dep_count']}]:")
+        for _ in range(10):
+            t = d["tasks"][ctx["tidx"][r]]
+            print(f"       {ctx['lab'][r]:24s} {str(where(t, d['tiles'], d['bp'])):22s} pushed {ctx['pushed'][r] - core_end:+8.1f} "
+                  f"claim {ctx['claim'][r] - core_end:+8.1f} done {ctx['done'][r] - core_end:+8.1f}")
+            best, bt, bchain = None, -1e18, False
+            for kk in range(t["dep_begin"], t["dep_begin"] + t["dep_count"] + t["dep2_count"]):
+                q = deps[kk]
+                e = events.get((int(q["counter"]), 0), [])
+                if q["value"] <= 0:
+                    continue
+                if len(e) < q["value"]:
+                    bchain = True  # produced by a chain step (not in the task records)
+                    continue
+                if e[q["value"] - 1][0] > bt:
+                    best, bt = e[q["value"] - 1][1], e[q["value"] - 1][0]
+            if best is None:
+                print("       <- chain step" if bchain else "       <- (start)")
+                break
+            if bchain:
+                print(f"         (also waits on a chain step)")
+            r = best
 
 
 def report(path):
@@ -207,6 +245,7 @@ def report(path):
         if len(w):
             print(f"  {name} queue wait (claim - pushed): mean {w.mean():.2f} us, p50 {np.median(w):.2f}, p90 "
                   f"{np.percentile(w, 90):.2f}, max {w.max():.1f}")
+    d["_ctx"] = dict(tidx=tidx, lab=lab, pushed=pushed, claim=claim, done=done)
     chain_deps_report(d, events, t0)
     r = int(np.argmax(done))
     path_seq = []
