@@ -262,7 +262,7 @@ static std::shared_ptr<DevPlan> upload_plan(DataflowPlan&& host, int device, cud
   d->host = std::move(host);
   d->device = device;
   d->grid = dataflow_grid(device);
-  if (d->grid <= d->host.q0.workers) throw Error(kErrCuda, "persistent grid too small for the critical queue");
+  if (kWorkers * d->grid <= d->host.q0.workers) throw Error(kErrCuda, "persistent grid too small for the critical queue");
   d->tasks.upload(d->host.tasks, s);
   d->segs.upload(d->host.segs, s);
   d->deps.upload(d->host.deps, s);

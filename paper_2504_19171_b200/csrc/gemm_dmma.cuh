@@ -27,7 +27,17 @@
 namespace tib {
 
 constexpr int kStages = 4;
-constexpr int kGemmThreads = 128;
+constexpr int kGemmThreads = 128;  // threads of one worker (4 warps)
+constexpr int kWorkers = 2;         // workers per CTA (one CTA per SM)
+
+// Worker-local thread index and barrier: each CTA runs kWorkers independent
+// task loops on its halves, synchronised by named barrier 1 + half (barrier
+// 0 stays the whole CTA).
+__device__ __forceinline__ int wtid() { return threadIdx.x & (kGemmThreads - 1); }
+__device__ __forceinline__ int whalf() { return threadIdx.x / kGemmThreads; }
+__device__ __forceinline__ void wsync() {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + static_cast<int>(threadIdx.x / kGemmThreads)), "n"(kGemmThreads) : "memory");
+}
 constexpr int kLdN = kBK + 4;   // [row][k] layout stride (doubles)
 constexpr int kLdT = kBM + 4;   // [k][row] layout stride (doubles)
 constexpr int kStageDoubles = (kBM * kLdN > kBK * kLdT ? kBM * kLdN : kBK * kLdT);
@@ -146,7 +156,7 @@ struct LocalSegs {
 // instead of per fragment.
 template <class Src>
 __device__ __forceinline__ void gemm_mainloop(const RTask& t, const Src& src, double* smem, double (&acc)[4][4][2]) {
-  const int tid = threadIdx.x;
+  const int tid = wtid();
   const int lane = tid & 31, warp = tid >> 5;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   const int fr = lane >> 2, fc = lane & 3;
@@ -197,7 +207,7 @@ __device__ __forceinline__ void gemm_mainloop(const RTask& t, const Src& src, do
   bool negated = false;
   for (int it = 0; it < nchunks; ++it) {
     cp_async_wait<kStages - 2>();
-    __syncthreads();
+    wsync();
     {
       const int nx = it + kStages - 1;
       if (nx < nchunks) {
@@ -260,16 +270,16 @@ __device__ __forceinline__ void gemm_mainloop(const RTask& t, const Src& src, do
         acc[i][j][1] = -acc[i][j][1];
       }
   }
-  __syncthreads();  // every warp is done with the ring before the next task refills it
+  wsync();  // every warp is done with the ring before the next task refills it
 }
 
 // Position of fragment (i, j, h) of the calling thread in the 64 x 64 block.
 __device__ __forceinline__ int frag_row(int i) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = wtid() >> 5;
   return (warp >> 1) * 32 + i * 8 + (lane >> 2);
 }
 __device__ __forceinline__ int frag_col(int j) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = wtid() >> 5;
   return (warp & 1) * 32 + j * 8 + (lane & 3) * 2;
 }
 
@@ -307,7 +317,7 @@ __device__ __forceinline__ void gemm_epilogue(const RTask& t, const double (&acc
       }
     }
   }
-  __syncthreads();
+  wsync();
 }
 
 // Split-K: a part's accumulators -> its 64 x 64 scratch slot (row-major).
