@@ -351,7 +351,7 @@ static const char* trace_prefix() {
 static std::atomic<int> g_trace_seq{0};
 
 static void write_trace(DevPlan& P, int batch, unsigned long long* d_trace, cudaStream_t s) {
-  const size_t n = (P.host.tasks.size() + P.host.chain.size()) * batch * 4;
+  const size_t n = (P.host.tasks.size() + 2 * P.host.chain.size()) * batch * 4;  // tasks, chain steps (worker 0, worker 1)
   std::vector<unsigned long long> h(n);
   CK(cudaMemcpyAsync(h.data(), d_trace, n * 8, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
@@ -416,6 +416,13 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
   a.missing = e.sched + 128 + 256;
   a.chain = P.chain.p;
   a.dedicate = batch <= env_int("TIB_DEDICATE_MAX_BATCH", 4) ? 1 : 0;
+  // eight-warp chains: the chain task is q0 task 0 and initially ready, so q0
+  // items 0 .. batch-1 are the chains; they run on CTAs 0 .. batch-1
+  a.chain8 = (a.dedicate && !P.host.chain.empty() && !P.host.init0.empty() && P.host.init0[0] == 0 &&
+              P.host.tasks[0].kind == kChainTask && batch <= P.grid && env_int("TIB_CHAIN8", 0) != 0)
+                 ? 1
+                 : 0;
+  if (a.chain8) a.dedicate = 0;
   a.poll_uploads = poll ? 1 : 0;
   a.slots0 = a.missing + nt * batch;
   a.slots1 = a.slots0 + static_cast<size_t>(P.host.q0.count) * batch;
@@ -447,7 +454,7 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
   }
   if (trace_prefix()) {
     unsigned long long* d_trace = nullptr;
-    const size_t n = (nt + P.host.chain.size()) * batch * 4;
+    const size_t n = (nt + 2 * P.host.chain.size()) * batch * 4;
     CK(cudaMallocAsync(reinterpret_cast<void**>(&d_trace), n * 8, s));
     CK(cudaMemsetAsync(d_trace, 0, n * 8, s));
     a.trace = d_trace;

@@ -41,7 +41,10 @@ def load(path):
         rec = np.frombuffer(f.read(), np.uint64).reshape(-1, 4)
     chain = rec[ntask * batch:]
     rec = rec[:ntask * batch]
-    return dict(chain=chain, chain_tasks=chain_tasks,ntask=ntask, batch=batch, nq0=nq0, nb=nb, tasks=tasks, deps=deps, sigs=sigs, segs=segs, rec=rec,
+    hchain = None
+    if len(chain) == 2 * nchain * batch:  # eight-warp chain: worker 1's records follow
+        chain, hchain = chain[:nchain * batch], chain[nchain * batch:]
+    return dict(chain=chain, hchain=hchain, chain_tasks=chain_tasks,ntask=ntask, batch=batch, nq0=nq0, nb=nb, tasks=tasks, deps=deps, sigs=sigs, segs=segs, rec=rec,
                 tiles=tiles, bp=bp)
 
 
@@ -102,6 +105,13 @@ def chain_report(d, t0):
         m = pos == k
         print(f"    block {k} of the tile: leaf core {core_t[m].mean():.2f} us, fat wait {fat_wait[m].mean():.2f}, "
               f"rest to next step {np.nanmean((nxt - core - fat_wait)[m]):.2f}, step {np.nanmean((nxt - start)[m]):.2f}")
+    if d.get("hchain") is not None:
+        hc = d["hchain"].astype(np.float64)[ok] / 1e3 - t0
+        s0, s1, s2, s3 = hc[:, 0], hc[:, 1], hc[:, 2], hc[:, 3]
+        has2 = hc[:, 2] > 0
+        print(f"    worker 1: S0 seen {np.mean(s0 - core):+.2f} us after the leaf, stores {np.mean(s1 - s0):.2f}, "
+              f"S2 seen {np.mean((s2 - s1)[has2]):.2f} after, 2nd signals {np.mean((s3 - s2)[has2]):.2f}; "
+              f"S1 published {np.nanmean(nxt - s1):.2f} us before the next step")
     first = np.arange(n) % nb == 0
     if first.any():
         print(f"    tile-first steps: dep wait mean {dep_wait[first].mean():.2f} us (total {dep_wait[first].sum() / 1e3:.1f} ms); "
@@ -121,14 +131,14 @@ def chain_deps_report(d, events, t0):
     lat = {}
     nb = d["nb"]
     for si, st in enumerate(tasks_chain):
-        if not (st["mode"] & 4 or si % nb == 0) or ch[si, 2] <= 0:
+        if ch[si, 2] <= 0:
             continue
         core_end = ch[si, 2] - t0
         for k in range(st["dep_begin"] + st["dep_count"], st["dep_begin"] + st["dep_count"] + st["dep2_count"]):
             dp = deps[k]
             ev = events.get((int(dp["counter"]), 0), [])
             if dp["value"] > 0 and len(ev) >= dp["value"]:
-                key = ("boundary" if st["mode"] & 4 else "block0", k - st["dep_begin"] - st["dep_count"])
+                key = ("boundary" if st["mode"] & 4 else f"block{si % nb}", k - st["dep_begin"] - st["dep_count"])
                 lat.setdefault(key, []).append(ev[dp["value"] - 1][0] - core_end)
     for k, v in sorted(lat.items()):
         v = np.array(v)
@@ -139,10 +149,15 @@ def chain_deps_report(d, events, t0):
     bsteps = [si for si, st in enumerate(tasks_chain) if st["mode"] & 4 and ch[si, 2] > 0]
     if not bsteps or ctx is None:
         return
-    si = bsteps[len(bsteps) // 2]
+    for si in (bsteps[len(bsteps) // 2], bsteps[len(bsteps) // 2] - 4):
+        walk_step(d, events, ctx, tasks_chain, ch, si, t0)
+
+
+def walk_step(d, events, ctx, tasks_chain, ch, si, t0):
+    deps = d["deps"]
     st = tasks_chain[si]
     core_end = ch[si, 2] - t0
-    print(f"    boundary step {si}: producers of its second-phase deps (times us relative to its leaf end):")
+    print(f"    chain step {si} (mode {int(st['mode'])}): producers of its second-phase deps (us relative to its leaf end):")
     for k in range(st["dep_begin"] + st["dep_count"], st["dep_begin"] + st["dep_count"] + st["dep2_count"]):
         dp = deps[k]
         ev = events.get((int(dp["counter"]), 0), [])
@@ -150,7 +165,7 @@ def chain_deps_report(d, events, t0):
             continue
         r = ev[dp["value"] - 1][1]
         print(f"     dep2[{k - st['dep_begin'] - st['dep_count']}]:")
-        for _ in range(10):
+        for _ in range(6):
             t = d["tasks"][ctx["tidx"][r]]
             print(f"       {ctx['lab'][r]:24s} {str(where(t, d['tiles'], d['bp'])):22s} pushed {ctx['pushed'][r] - core_end:+8.1f} "
                   f"claim {ctx['claim'][r] - core_end:+8.1f} done {ctx['done'][r] - core_end:+8.1f}")
