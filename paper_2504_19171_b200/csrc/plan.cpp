@@ -20,6 +20,7 @@ struct Builder {
   DataflowPlan& P;
   std::vector<DTask> all;
   std::vector<unsigned char> queue;
+  std::vector<int> conv;  // emission index -> index after the chain conversion
   explicit Builder(DataflowPlan& p) : P(p) {}
 
   DTask& add(int q, const std::vector<Dep>& deps, const std::vector<int>& sigs, const std::vector<Dep>& deps2 = {}) {
@@ -68,10 +69,13 @@ struct Builder {
       std::vector<DTask> rest;
       std::vector<unsigned char> rq;
       P.chain.clear();
+      conv.assign(all.size(), -1);
+      const bool any_leaf = std::any_of(all.begin(), all.end(), [](const DTask& t) { return t.kind == kLeafTask; });
       for (size_t i = 0; i < all.size(); ++i) {
         if (all[i].kind == kLeafTask) {
           P.chain.push_back(all[i]);
         } else {
+          conv[i] = static_cast<int>(rest.size()) + (any_leaf ? 1 : 0);
           rest.push_back(all[i]);
           rq.push_back(queue[i]);
         }
@@ -106,6 +110,10 @@ struct Builder {
         P.tasks.push_back(all[i]);
       }
     P.q0 = QueueDesc{0, n0, n0 > 0 ? crit_workers : 0, 0};
+    if (chain)  // chain steps reference tasks by emission index: to final indices
+      for (DTask& s : P.chain)
+        for (int* f : {&s.aux0, &s.aux1, &s.pad2})
+          if (*f >= 0) *f = pos[static_cast<size_t>(conv[static_cast<size_t>(*f)])];
     P.q1 = QueueDesc{n0, static_cast<int>(P.tasks.size()) - n0, 0, 0};
     finalize_waiters();
     return pos;
@@ -549,17 +557,40 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
       }
     };
     for (int kk = 0; kk < nb; ++kk) {
+      const int li = static_cast<int>(B.all.size());
       leaf(kk);
+      if (chain && kk >= 1 && kk + 1 < nb) B.all[static_cast<size_t>(li)].mode |= 8;
       if (kk + 1 < nb && !fat_leaf) {
         paneld(kk + 1, kk);
         traild(kk + 1, kk + 1, kk);
       }
       for (int k = 0; k < kk; ++k) xrow(kk, k);
       for (int k = 0; k <= kk && kk + 1 < nb; ++k) tterm(kk + 1, k, kk);
-      for (int i = kk + 2; i < nb; ++i) paneld(i, kk);
+      // chain lookahead (eight-warp chain): the panel block L(kk+2, kk) and
+      // its kk terms on blocks (kk+2, kk+1) and (kk+2, kk+2) -- the next
+      // step's second-phase operands -- are formed by the chain itself; the
+      // tasks stay in the plan for the other executors, marked chain-owned
+      // (pad2) and referenced from the step (aux0, aux1, pad2: emission index)
+      int la[3] = {-1, -1, -1};
+      for (int i = kk + 2; i < nb; ++i) {
+        if (chain && i == kk + 2) la[0] = static_cast<int>(B.all.size());
+        paneld(i, kk);
+      }
       for (int p = kk + 1; p < nb; ++p)
         for (int i = p; i < nb; ++i)
-          if (!(i == kk + 1 && p == kk + 1)) traild(i, p, kk);
+          if (!(i == kk + 1 && p == kk + 1)) {
+            if (chain && i == kk + 2 && p == kk + 1) la[1] = static_cast<int>(B.all.size());
+            if (chain && i == kk + 2 && p == kk + 2) la[2] = static_cast<int>(B.all.size());
+            traild(i, p, kk);
+          }
+      {
+        DTask& lt = B.all[static_cast<size_t>(li)];
+        lt.aux0 = la[0];
+        lt.aux1 = la[1];
+        lt.pad2 = la[2];
+        for (int x : la)
+          if (x >= 0) B.all[static_cast<size_t>(x)].pad2 = 1;
+      }
       for (int kk2 = kk + 2; kk2 < nb; ++kk2)
         for (int k = 0; k <= kk; ++k) tterm(kk2, k, kk);
       if (tail0 && !bnd_col) {
