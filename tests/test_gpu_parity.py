@@ -156,6 +156,19 @@ def test_streamed_upload_is_bitwise_identical(tib, monkeypatch):
     assert streamed.logdet() == upfront.logdet()
 
 
+@pytest.mark.parametrize("b", [256, 512])
+def test_eight_warp_chain_is_bitwise_identical(tib, monkeypatch, b):
+    """The experimental eight-warp chain (TIB_CHAIN8=1: a helper worker stores
+    each leaf, raises the chain's signals and forms the lookahead products)
+    performs the same operations in the same order as the default chain."""
+    m = tib.generate(9000, 900, 60, 1.0, seed=29, tile_size=b)
+    ref = tib.selected_inverse(m, "pattern")
+    monkeypatch.setenv("TIB_CHAIN8", "1")
+    alt = tib.selected_inverse(m, "pattern")
+    assert alt.checksum == ref.checksum
+    assert alt.logdet() == ref.logdet()
+
+
 @pytest.mark.parametrize("cfg", [
     ("medium", 100000, 1000, 100, 256, 6.955199016515e05, 9.580956859578e01),
     ("large", 200000, 2000, 200, 512, 1.529607821236e06, 9.582054347524e01),
