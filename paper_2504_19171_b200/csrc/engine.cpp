@@ -254,7 +254,7 @@ static int env_int(const char* name, int dflt) {
 static int crit_workers(bool factor) {
   const int all = env_int("TIB_CRIT_WORKERS", 0);
   if (all > 0) return all;
-  return factor ? env_int("TIB_CRIT_WORKERS_FACTOR", 40) : env_int("TIB_CRIT_WORKERS_P2", 12);
+  return factor ? env_int("TIB_CRIT_WORKERS_FACTOR", 56) : env_int("TIB_CRIT_WORKERS_P2", 12);
 }
 
 static std::shared_ptr<DevPlan> upload_plan(DataflowPlan&& host, int device, cudaStream_t s) {
