@@ -224,7 +224,8 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
       s_slots += nb;
     }
   const int m_slots = bnd ? nb : 0;  // M_q = X_q L(j, j)[q, q-1] per block column
-  const int slots_per_col = 2 * panel_slots + 2 * upd_slots + s_slots + m_slots;
+  const int sp_slots = bnd ? 2 * NB2 : 0;  // the two parts of each S-trick panel block
+  const int slots_per_col = 2 * panel_slots + 2 * upd_slots + s_slots + m_slots + sp_slots;
   constexpr int kRing = 4;  // columns of partial slots in flight (see the reuse argument below)
   // counter spaces
   const long cAord = 0, cAfin = cAord + T * NB2, cLblk = cAfin + T, cLfin = cLblk + T * NB2,
@@ -543,17 +544,30 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
         ++t.seg_count;
         P.task_flops += 2.0 * kB * kB * kB;
       };
+      // two split parts, so the row's hop is only the last one (K = 64):
+      //   part 0: (A - S) X_q^T  (X_q and S^q_p exist early)
+      //   part 1: -L(k0, j)[p, q-1] M_q^T  (the previous block of the row)
       for (int p = q == nb - 1 ? 1 : 0; p < nb; ++p) {
         const bool has_s = s_terms(q, p) >= 1;
-        std::vector<Dep> d{{xblk(j, q, q), 1}, {afin(sk0), Uk0 * NB2}, {mdone(j, q), 1}, {lblk(sk0, p, q - 1), 1}};
-        if (has_s) d.push_back({sdone(j, q, p), 1});
-        DTask& t = B.add(0, d, {lblk(sk0, p, q), lfin(sk0)});
-        t.kind = kGemmTask;
-        t.c_store = kStoreL;
-        t.c_off = blk_off(sk0, bp, p, q);
-        B.seg(t, kStoreA, blk_off(sk0, bp, p, q), kStoreP1, xd, 0, kB, kTransB);
-        if (has_s) scratch_seg(t, s_off(q, p), kStoreP1, xd, bp);
-        scratch_seg(t, blk_off(sk0, bp, p, q - 1), kStoreScratch, m_off(q), kB, kStoreL, bp);
+        const int slot = 2 * panel_slots + 2 * upd_slots + s_slots + m_slots + 2 * (q * nb + p);
+        auto part = [&](int r, const std::vector<Dep>& d) -> DTask& {
+          DTask& t = B.add(0, d, {lblk(sk0, p, q), lfin(sk0)});
+          t.kind = kSplitTask;
+          t.c_store = kStoreL;
+          t.c_off = blk_off(sk0, bp, p, q);
+          t.p_off = static_cast<long long>(t_doubles) +
+                    (static_cast<long long>(j % kRing) * slots_per_col + slot) * kB * kB;
+          t.aux0 = static_cast<int>(cArrive + static_cast<long>(j) * slots_per_col + slot);
+          t.aux1 = (r << 8) | 2;
+          return t;
+        };
+        std::vector<Dep> d0{{xblk(j, q, q), 1}, {afin(sk0), Uk0 * NB2}};
+        if (has_s) d0.push_back({sdone(j, q, p), 1});
+        DTask& t0 = part(0, d0);
+        B.seg(t0, kStoreA, blk_off(sk0, bp, p, q), kStoreP1, xd, 0, kB, kTransB);
+        if (has_s) scratch_seg(t0, s_off(q, p), kStoreP1, xd, bp);
+        DTask& t1 = part(1, {{mdone(j, q), 1}, {lblk(sk0, p, q - 1), 1}});
+        scratch_seg(t1, blk_off(sk0, bp, p, q - 1), kStoreScratch, m_off(q), kB, kStoreL, bp);
       }
     };
     for (int kk = 0; kk < nb; ++kk) {

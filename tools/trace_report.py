@@ -105,7 +105,7 @@ def chain_report(d, t0):
         m = pos == k
         print(f"    block {k} of the tile: leaf core {core_t[m].mean():.2f} us, fat wait {fat_wait[m].mean():.2f}, "
               f"rest to next step {np.nanmean((nxt - core - fat_wait)[m]):.2f}, step {np.nanmean((nxt - start)[m]):.2f}")
-    if d.get("hchain") is not None:
+    if d.get("hchain") is not None and d["hchain"][:, 0].any():
         hc = d["hchain"].astype(np.float64)[ok] / 1e3 - t0
         s0, s1, s2, s3 = hc[:, 0], hc[:, 1], hc[:, 2], hc[:, 3]
         has2 = hc[:, 2] > 0
