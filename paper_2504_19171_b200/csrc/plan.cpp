@@ -619,7 +619,9 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
           s_panel(kk);
         }
         const int r = upd_part_at(kk);
-        if (r >= 0) update_split(0, 0, r, u00, 0, 2 * panel_slots, 1);
+        // the next diagonal tile's updates (all but block (0, 0)) go to the bulk
+        // queue: in q0 their bursts at odd steps delayed the chain's helpers
+        if (r >= 0) update_split(0, 0, r, u00, 1, 2 * panel_slots, 1);
         // block (0, 0): its clipped last part goes out one step early
         if (upd_parts > 1) {
           for (int rr = 0; rr < upd_parts; ++rr) {
