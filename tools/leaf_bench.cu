@@ -10,7 +10,7 @@ __global__ void leaf_bench_kernel(const double* A, double* L, double* X, DevStat
   extern __shared__ __align__(16) double smem[];
   long long t0 = clock64();
   for (int r = 0; r < reps; ++r)
-    leaf_potrf_inv(A, 64, L, X, 64, true, 64, 0, st, ld, smem, nullptr, nullptr, nullptr);
+    leaf_potrf_inv<true>(A, 64, L, X, 64, 64, 0, st, ld, smem);
   long long t1 = clock64();
   if (threadIdx.x == 0) cyc[0] = (t1 - t0) / reps;
 }
