@@ -37,12 +37,14 @@ CONFIGS = {
     "small": (10000, 200, 50, 128),
     "medium": (100000, 1000, 100, 256),
     "large": (200000, 2000, 200, 512),
+    "batch": (50000, 500, 50, 128),  # BASELINE config 5: 64 such matrices, split over the GPUs
 }
+BATCH_TOTAL = {"batch": 64}  # matrices per step over all GPUs (config 5, seeds 1000..1063)
 METRIC = "factorize+selinv FP64 TFLOP/s (reference task model), whole job"
 PEAK_FILE = os.path.join(ROOT, "profiles", "r01_fp64_peak.jsonl")
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "dataflow_traffic.json")
 REF_DRIVER = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
-REF_SAMPLE_N = {"small": 10000, "medium": 12000, "large": 12000}  # bounded CPU sample (same w, t, b)
+REF_SAMPLE_N = {"small": 10000, "medium": 12000, "large": 12000, "batch": 50000}  # bounded CPU sample (same w, t, b)
 
 
 def fp64_peak():
@@ -202,16 +204,20 @@ def main():
     import paper_2504_19171_b200 as tib
 
     n, w, t, b = CONFIGS[args.config]
-    seed = 42 + rank
-    m = tib.generate(n, w, t, 1.0, seed=seed, tile_size=b)
+    per = max(1, BATCH_TOTAL.get(args.config, world) // world)  # matrices per GPU per step
+    if args.config in BATCH_TOTAL:
+        ms = [tib.generate(n, w, t, 1.0, seed=1000 + rank * per + k, tile_size=b) for k in range(per)]
+    else:
+        ms = [tib.generate(n, w, t, 1.0, seed=42 + rank, tile_size=b)]
+    m = ms[0]
     f_fact, f_p1, f_p2 = tib.task_flops(m)
-    flops = f_fact + f_p1 + f_p2
+    flops = (f_fact + f_p1 + f_p2) * per  # per GPU per step
     _, _, stored_tiles = m.n, m.tile_size, m.stored_tiles
-    h2d = stored_tiles * b * b * 8
-    d2h = n * 8
+    h2d = stored_tiles * b * b * 8 * per
+    d2h = n * 8 * per
 
     # ---- device-resident timing: K fused sweeps, CUDA events on the library stream
-    res = tib.Resident(m, device=local)
+    res = tib.Resident(m if per == 1 else ms, device=local)
     res.run(args.warmup)
     torch.cuda.synchronize()
     barrier()
@@ -226,17 +232,21 @@ def main():
     value = world * flops / (ms_step / 1e3) / 1e12
 
     # ---- end to end through the public API, host buffers, H2D + D2H inside
-    r = tib.selected_inverse(m, "pattern", device=local)
-    r.diagonal()
-    del r
+    def public_call():
+        if per == 1:
+            r = tib.selected_inverse(m, "pattern", device=local)
+            _ = r.diagonal(), r.logdet()
+            del r
+        else:  # marginal variances + logdet of every matrix of the batch, one batched call
+            _ = tib.selected_inverse_batch(ms, device=local)
+
+    public_call()
     torch.cuda.synchronize()
     barrier()
     t0 = time.perf_counter()
     e2e_steps = max(1, min(args.steps, 3))
     for _ in range(e2e_steps):
-        r = tib.selected_inverse(m, "pattern", device=local)
-        _ = r.diagonal(), r.logdet()
-        del r
+        public_call()
     torch.cuda.synchronize()
     e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
     barrier()
@@ -255,19 +265,24 @@ def main():
         pass
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (bit-exact reference generator, density 1, seed 42+rank)",
-        "config": {"workload": f"{args.config} arrowhead n={n} w={w} t={t} b={b}: fused factorize + selected "
-                               f"inversion (pattern) + marginal variances + logdet per matrix",
-                   "n": n, "bandwidth": w, "thickness": t, "tile": b, "matrices_per_gpu_per_step": 1,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong" if args.config in BATCH_TOTAL else "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (bit-exact reference generator, density 1, " +
+                ("seeds 1000..1063 over the GPUs)" if args.config in BATCH_TOTAL else "seed 42+rank)"),
+        "config": {"workload": f"{args.config} arrowhead n={n} w={w} t={t} b={b}"
+                               + (f" x{per} matrices per GPU (one batched launch per sweep)" if per > 1 else "")
+                               + ": fused factorize + selected inversion (pattern) + marginal variances + logdet "
+                                 "per matrix",
+                   "n": n, "bandwidth": w, "thickness": t, "tile": b, "matrices_per_gpu_per_step": per,
                    "parallelism": f"independent matrices per GPU (x{world})",
                    "l2": "inputs larger than L2 (tile store %.1f GB per copy)" % (h2d / 1e9),
                    "task_model_gflop": flops / 1e9, "executed_gflop": info["executed_flops"] / 1e9},
-        "seconds_per_matrix": ms_step / 1e3,
+        "seconds_per_matrix": ms_step / 1e3 / per,
         "ms_factorize_sweep": ms_fact, "ms_phase2_sweep": ms_p2,
         "logdet": info["logdet"],
         "e2e": {"value": e2e, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
-                "seconds_per_matrix": e2e_s},
+                "seconds_per_matrix": e2e_s / per},
         "gpu_launches": int(info["kernel_launches_per_rep"]) * args.steps,
         "roofline": {"bound": "tensor", "achieved": per_gpu, "peak": peak, "unit": "TFLOP/s",
                      "frac": per_gpu / peak, "traffic": traffic, "peak_source": peak_src,

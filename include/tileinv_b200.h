@@ -143,6 +143,9 @@ int tib_plan_export(tib_matrix m, int preset, const long* rows, const long* cols
  * inversion (pattern) `reps` times.  Times are CUDA events on the library
  * stream: total over reps and the two sweeps of the last rep.                */
 int tib_resident_create(tib_matrix m, int device, tib_resident* out);
+/* The same for `count` matrices of one tile pattern, run as one batch (every
+ * sweep is one launch for the whole batch; BASELINE config 5).               */
+int tib_resident_create_batch(const tib_matrix* ms, int count, int device, tib_resident* out);
 int tib_resident_run(tib_resident r, int reps, double* ms_total, double* ms_factor, double* ms_phase2);
 int tib_resident_info(tib_resident r, double* task_model_flops, double* executed_flops, double* logdet,
                       long* kernel_launches_per_rep);

@@ -485,9 +485,14 @@ class Resident:
     times `reps` fused factorize + selected-inversion sweeps with CUDA events on
     the library stream (the bench's device-side measurement)."""
 
-    def __init__(self, matrix: Matrix, device: int = 0):
+    def __init__(self, matrix, device: int = 0):
         h = _new_handle()
-        _check(lib.tib_resident_create(matrix._h, device, C.byref(h)))
+        if isinstance(matrix, Matrix):
+            _check(lib.tib_resident_create(matrix._h, device, C.byref(h)))
+        else:  # a batch of matrices sharing one tile pattern
+            ms = list(matrix)
+            arr = (C.c_void_p * len(ms))(*[m._h.value for m in ms])
+            _check(lib.tib_resident_create_batch(arr, len(ms), device, C.byref(h)))
         self._h = h
 
     def run(self, reps: int = 1):

@@ -66,6 +66,7 @@ SIGNATURES = {
     "tib_bench_resident": [_p, _i, _i, _i, _pd, _pd, _pd, _pd],
     "tib_plan_export": [_p, _i, _pl, _pl, _l, _i, _i, _pd, _p, _p, _p, _p],
     "tib_resident_create": [_p, _i, _pp],
+    "tib_resident_create_batch": [_pp, _i, _i, _pp],
     "tib_resident_run": [_p, _i, _pd, _pd, _pd],
     "tib_resident_info": [_p, _pd, _pd, _pd, _pl],
     "tib_resident_free": [_p],

@@ -1158,6 +1158,7 @@ int tib_plan_export(tib_matrix m, int preset, const long* rows, const long* cols
 
 struct tib_resident_s {
   int device = 0;
+  int count = 1;  // matrices (one tile pattern), run as one batch
   Layout layout;
   std::shared_ptr<FactorPlan2> fp;
   std::shared_ptr<Phase2Plan> p2;
@@ -1171,12 +1172,21 @@ struct tib_resident_s {
 extern "C" {
 
 int tib_resident_create(tib_matrix m, int device, tib_resident* out) {
+  return tib_resident_create_batch(&m, 1, device, out);
+}
+
+int tib_resident_create_batch(const tib_matrix* ms, int count, int device, tib_resident* out) {
   return guarded([&] {
-    need(m, "matrix");
+    if (count < 1 || !ms) throw Error(kErrInvalidArgument, "batch needs at least one matrix");
+    const MatrixObj* m = need(ms[0], "matrix");
+    for (int k = 1; k < count; ++k)
+      if (!(need(ms[k], "matrix")->pattern == m->pattern) || ms[k]->layout.n != m->layout.n)
+        throw Error(kErrInvalidArgument, "batched matrices must share one tile pattern");
     DeviceRt& rt = runtime(device);
     cudaStream_t s = rt.stream;
     auto r = std::make_unique<tib_resident_s>();
     r->device = device;
+    r->count = count;
     r->layout = m->layout;
     r->fp = factor_plan_for(m->pattern, device, s);
     const Pattern& F = r->fp->sym.filled;
@@ -1185,15 +1195,21 @@ int tib_resident_create(tib_matrix m, int device, tib_resident* out) {
     const Closure sel = symbolic_inversion(select_tiles(F.layout(), F, req), F);
     r->p2 = phase2_plan_for(F, sel, device, s);
     const Flops fl = count_flops(r->fp->sym, &r->p2->sel);
-    r->model_flops = fl.total();
+    r->model_flops = fl.total() * count;
     const size_t tile = static_cast<size_t>(r->fp->bp) * r->fp->bp;
-    alloc_factor_stores(r->st, *r->fp, 1, device, s, r->p2->flow->host.counters, r->p2->flow->host.scratch_doubles);
-    r->A0 = DevBuf(F.size() * tile, device, s);
-    upload_matrix(*m, F, r->fp->bp, r->A0.p, s);
-    r->Sg = DevBuf(r->p2->sel.closure.size() * tile, device, s);
-    r->var = DevBuf(static_cast<size_t>(m->layout.N) * r->fp->bp, device, s);
-    r->tables = {make_table(r->st.A.p, r->st.L.p, r->st.P1.p, r->Sg.p, r->var.p, r->st.scratch.p, r->st.logdet.p,
-                            r->st.status.p, r->st.ctr(0))};
+    const size_t T = F.size(), C = r->p2->sel.closure.size(), nv = static_cast<size_t>(m->layout.N) * r->fp->bp;
+    alloc_factor_stores(r->st, *r->fp, count, device, s, r->p2->flow->host.counters,
+                        r->p2->flow->host.scratch_doubles);
+    r->A0 = DevBuf(T * tile * count, device, s);
+    for (int k = 0; k < count; ++k) upload_matrix(*ms[k], F, r->fp->bp, r->A0.p + T * tile * k, s);
+    r->Sg = DevBuf(C * tile * count, device, s);
+    r->var = DevBuf(nv * count, device, s);
+    for (int k = 0; k < count; ++k)
+      r->tables.push_back(make_table(r->st.A.p + T * tile * k, r->st.L.p + T * tile * k, r->st.P1.p + T * tile * k,
+                                     r->Sg.p + C * tile * k, r->var.p + nv * k,
+                                     r->st.scratch.p + r->st.scratch_stride * k,
+                                     r->st.logdet.p + r->fp->flow->host.logdet_doubles * k, r->st.status.p + k,
+                                     r->st.ctr(k)));
     CK(cudaStreamSynchronize(s));
     *out = r.release();
   });
@@ -1224,9 +1240,9 @@ int tib_resident_run(tib_resident r, int reps, double* ms_total, double* ms_fact
       total += tf + tp;
     }
     for (auto& e : ev) cudaEventDestroy(e);
-    std::vector<double> parts(r->fp->flow->host.logdet_doubles);
+    std::vector<double> parts(r->fp->flow->host.logdet_doubles);  // matrix 0's
     CK(cudaMemcpyAsync(parts.data(), r->st.logdet.p, parts.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
-    check_status(r->st.status, 1, r->layout, s);
+    check_status(r->st.status, r->count, r->layout, s);
     r->logdet = reduce_logdet(parts.data(), r->layout.N, r->fp->nb);
     if (ms_total) *ms_total = total;
     if (ms_factor) *ms_factor = tf;
@@ -1238,7 +1254,7 @@ int tib_resident_info(tib_resident r, double* model, double* executed, double* l
   return guarded([&] {
     need(r, "resident");
     if (model) *model = r->model_flops;
-    if (executed) *executed = r->fp->flow->host.task_flops + r->p2->flow->host.task_flops;
+    if (executed) *executed = (r->fp->flow->host.task_flops + r->p2->flow->host.task_flops) * r->count;
     if (logdet) *logdet = r->logdet;
     // per sweep: scheduler init + the persistent dataflow kernel (+ the zero-strip
     // kernel when the plan has strips)
