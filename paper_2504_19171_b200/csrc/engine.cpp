@@ -423,6 +423,13 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
                  ? 1
                  : 0;
   if (a.chain8) a.dedicate = 0;
+  a.static_chains = (!P.host.chain.empty() && !P.host.init0.empty() && P.host.init0[0] == 0 &&
+                     P.host.tasks[0].kind == kChainTask && batch <= P.grid)
+                        ? 1
+                        : 0;
+  // the chains' workers are reserved ones (worker 0 of the first CTAs): keep
+  // the plan's count of reserved workers for the chain's helpers
+  if (a.static_chains || a.chain8) a.q0.workers += batch;
   a.poll_uploads = poll ? 1 : 0;
   a.slots0 = a.missing + nt * batch;
   a.slots1 = a.slots0 + static_cast<size_t>(P.host.q0.count) * batch;

@@ -37,6 +37,7 @@ struct FlowArgs {
   int* sm_flags;       // [256]: SM hosts a running chain
   int dedicate;        // chains get their SM to themselves
   int chain8;          // chains run on both workers of CTAs 0 .. batch-1 (q0 items 0 .. batch-1 skipped)
+  int static_chains;   // chains run on worker 0 of CTAs 0 .. batch-1 (q0 items 0 .. batch-1 skipped)
   int poll_uploads;    // streamed upload: tasks wait for their A-store column (DTask::poll)
   unsigned long long* trace;
 };

@@ -135,12 +135,14 @@ def test_factor_path_and_determinism(tib, orc):
     assert elementwise(diag.diagonal(), ref["diag"]) <= TOL
 
 
-@pytest.mark.parametrize("count", [3, 6])  # 6 > TIB_DEDICATE_MAX_BATCH: chains share their SMs
+@pytest.mark.parametrize("count", [3, 6, 80])  # 6 > TIB_DEDICATE_MAX_BATCH: chains share their SMs;
+# 80 > the reserved critical workers: every chain still runs on its own worker
 def test_batch_matches_single(tib, count):
-    ms = [tib.generate(5000, 500, 50, 1.0, seed=1000 + k, tile_size=128) for k in range(count)]
+    b = 256 if count > 6 else 128
+    ms = [tib.generate(5000, 500, 50, 1.0, seed=1000 + k, tile_size=b) for k in range(count)]
     logdet, diag = tib.selected_inverse_batch(ms)
-    for k, m in enumerate(ms):
-        res = tib.selected_inverse(m, "pattern")
+    for k in (range(count) if count <= 6 else (0, 1, count - 2, count - 1)):
+        res = tib.selected_inverse(ms[k], "pattern")
         assert logdet[k] == res.logdet()
         assert np.array_equal(diag[k], res.diagonal())
 
