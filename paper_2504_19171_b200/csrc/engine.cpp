@@ -412,8 +412,7 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
   a.ntasks = static_cast<int>(nt);
   a.tables = e.tables;
   a.ctl = e.sched;
-  a.sm_flags = e.sched + 128;
-  a.missing = e.sched + 128 + 256;
+  a.missing = e.sched + 128 + 256;  // (ctl lines, 256 spare ints, then the per-task counts)
   a.chain = P.chain.p;
   a.dedicate = batch <= env_int("TIB_DEDICATE_MAX_BATCH", 4) ? 1 : 0;
   // eight-warp chains: the chain task is q0 task 0 and initially ready, so q0

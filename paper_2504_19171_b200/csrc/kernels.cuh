@@ -34,7 +34,6 @@ struct FlowArgs {
   int* slots1;   // q1.count x batch
   int* ctl;      // head0, tail0, head1, tail1 (128-byte apart)
   const DTask* chain;  // chain steps (kChainTask)
-  int* sm_flags;       // [256]: SM hosts a running chain
   int dedicate;        // chains get their SM to themselves
   int chain8;          // chains run on both workers of CTAs 0 .. batch-1 (q0 items 0 .. batch-1 skipped)
   int static_chains;   // chains run on worker 0 of CTAs 0 .. batch-1 (q0 items 0 .. batch-1 skipped)
