@@ -20,9 +20,18 @@ __global__ void chain_kernel(const double* A, const double* P, const double* Dn,
       __syncthreads();
     }
     const long long t0 = clock64();
-    leaf_potrf_inv<true>(mode == 0 ? A : nullptr, 64, L, X, 64, 64, 0, st, ld, smem);
+    if (mode == 4) {
+      // the sweep's pipelining: the previous step's D' tail on warps 2-3 during
+      // the first 32x32 sweep (operands: whatever SP / SA hold)
+      if (threadIdx.x < 64) leaf_first<true>(smem);
+      else chain_fat_tail(smem);
+      __syncthreads();
+      leaf_rest<true>(L, X, 64, 64, 0, st, ld, smem);
+    } else {
+      leaf_potrf_inv<true>(mode == 0 ? A : nullptr, 64, L, X, 64, 64, 0, st, ld, smem);
+    }
     const long long t1 = clock64();
-    if (mode == 2) {
+    if (mode == 2 || mode == 4) {
       chain_fat_prefetch(P, Dn, 64, smem);
       double* SX = smem + kLeaf * kLs;
       for (int idx = threadIdx.x; idx < kL2 * kL2; idx += kGemmThreads) SX[(idx / kL2) * kLs + kL2 + (idx % kL2)] = 0.0;
@@ -73,7 +82,7 @@ int main() {
   cudaMemcpy(dP, p.data(), 32768, cudaMemcpyHostToDevice);
   cudaMemset(st, 0xff, 8);
   cudaFuncSetAttribute(chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFlowSmemBytes);
-  for (int mode : {0, 1, 2, 0, 1, 2}) {
+  for (int mode : {0, 1, 2, 4, 0, 1, 2, 4}) {
     chain_kernel<<<1, 128, kFlowSmemBytes>>>(dA, dP, dA, dL, dX, dPo, st, dld, cyc, 50, mode);
     long long c[3];
     cudaMemcpy(c, cyc, 24, cudaMemcpyDeviceToHost);
