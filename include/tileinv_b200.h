@@ -57,6 +57,17 @@ int tib_device_count(int* count);
 /* generate_arrowhead (matgen.hpp:54, matgen.cpp:59-120), bit-exact values.  */
 int tib_matrix_generate(long n, long bandwidth, long thickness, double density, uint64_t seed,
                         int tile_size, tib_matrix* out);
+/* generate_arrowhead at density 1 ON THE DEVICE (generate.cu; values
+ * bit-identical to tib_matrix_generate and to the reference): the matrix
+ * lives as parameters, each sweep generates it straight into its A store (no
+ * host copy, no H2D).  Host-side accessors (tiles, write_mm, checksum)
+ * materialise the values from the device on first use.                      */
+int tib_matrix_generate_device(long n, long bandwidth, long thickness, uint64_t seed, int tile_size, int device,
+                               tib_matrix* out);
+/* payload_checksum (storage.cpp:34-48) of the matrix tiles: FNV-1a over the
+ * column-major tile keys and b*b payloads, equal to the reference's value
+ * for the same matrix.                                                       */
+int tib_matrix_checksum(tib_matrix m, uint64_t* out);
 /* from_dense (module.cpp:46-74): row-major n x n, lower triangle read.      */
 int tib_matrix_from_dense(long n, int tile_size, const double* a, tib_matrix* out);
 /* Tiles (i >= j), each b*b row-major, as a TileBlocks payload list.         */

@@ -16,6 +16,7 @@
 //          selection = diagonal | pattern | all | r,c;r,c;...
 //       -> <prefix>.diag.f64 (n doubles), <prefix>.sigma.f64 (closure tiles,
 //          column-major tile order, each b*b row-major) and a JSON line.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -119,8 +120,109 @@ static int symbolic_main(int argc, char** argv) {
   return 0;
 }
 
+// Golden summary of a selected inverse (ref_driver golden / golden_mm): the
+// reference's own numbers at the BASELINE configs, small enough to commit.
+//   <prefix>.diag.f64    diag(Sigma), n doubles (marginal variances)
+//   <prefix>.tstats.f64  per closure tile (column-major): Frobenius norm, sum,
+//                        weighted sum with w(r, c) = ((7 r + 13 c) mod 11) - 5
+//   <prefix>.blocks.f64  for each sampled tile: the leading s x s block and the
+//                        trailing s x s block of its valid region (s = min(64, b))
+//   stdout               JSON: logdet, trace, checksums, sampled tile list
+static int golden_run(const TiledSymmetricMatrix& m, int workers, const std::string& prefix) {
+  const long n = m.layout.n;
+  const int b = m.layout.b;
+  const auto t0 = Clock::now();
+  const FactorPlan plan = symbolic_cholesky(m.pattern);
+  TiledFactor factor = factorize(m, plan, workers);
+  double logdet = 0.0;
+  for (long r = 0; r < n; ++r) {
+    const auto& d = factor.blocks.at(static_cast<int>(r / b), static_cast<int>(r / b));
+    logdet += 2.0 * std::log(d[static_cast<std::size_t>(r % b) * b + (r % b)]);
+  }
+  const std::uint64_t msum = payload_checksum(m.blocks);
+  const std::uint64_t fsum = payload_checksum(factor.blocks);
+  const SelectedTileSet sel =
+      symbolic_inversion(select_tiles(factor.layout, factor.pattern, SelectionRequest::factor_pattern()),
+                         factor.pattern);
+  factor = phase1(std::move(factor), workers);
+  SelectedInverse sigma = phase2(factor, sel, workers);
+  const auto t1 = Clock::now();
+  const int N = m.layout.N;
+  std::vector<double> diag(static_cast<std::size_t>(n));
+  double trace = 0.0;
+  for (long r = 0; r < n; ++r) {
+    const auto& d = sigma.blocks.at(static_cast<int>(r / b), static_cast<int>(r / b));
+    diag[static_cast<std::size_t>(r)] = d[static_cast<std::size_t>(r % b) * b + (r % b)];
+    trace += diag[static_cast<std::size_t>(r)];
+  }
+  std::vector<double> stats;
+  std::vector<TileCoord> sampled;
+  for (const auto& [key, p] : sigma.blocks.map()) {
+    const int i = static_cast<int>(key & 0xffffffffu), j = static_cast<int>(key >> 32);
+    double fro = 0, sum = 0, wsum = 0;
+    for (int r = 0; r < b; ++r)
+      for (int c = 0; c < b; ++c) {
+        const double v = p[static_cast<std::size_t>(r) * b + c];
+        fro += v * v;
+        sum += v;
+        wsum += v * static_cast<double>(((7 * r + 13 * c) % 11) - 5);
+      }
+    stats.push_back(std::sqrt(fro));
+    stats.push_back(sum);
+    stats.push_back(wsum);
+    const bool pick = j >= N - 3 || j == N / 2 || (i == N - 1 && (j == 0 || j == N / 2 || j == N - 4));
+    if (pick) sampled.push_back({i, j});
+  }
+  const int s = b < 64 ? b : 64;
+  std::ofstream bl(prefix + ".blocks.f64", std::ios::binary);
+  for (const TileCoord& tc : sampled) {
+    const auto& p = sigma.blocks.at(tc.i, tc.j);
+    const long vr = std::min<long>(b, n - static_cast<long>(tc.i) * b), vc = std::min<long>(b, n - static_cast<long>(tc.j) * b);
+    for (int part = 0; part < 2; ++part) {
+      const long r0 = part ? vr - s : 0, c0 = part ? vc - s : 0;
+      for (long r = r0; r < r0 + s; ++r)
+        bl.write(reinterpret_cast<const char*>(p.data() + r * b + c0), static_cast<std::streamsize>(s * sizeof(double)));
+    }
+  }
+  std::ofstream dg(prefix + ".diag.f64", std::ios::binary);
+  dg.write(reinterpret_cast<const char*>(diag.data()), static_cast<std::streamsize>(diag.size() * sizeof(double)));
+  std::ofstream ts(prefix + ".tstats.f64", std::ios::binary);
+  ts.write(reinterpret_cast<const char*>(stats.data()), static_cast<std::streamsize>(stats.size() * sizeof(double)));
+  std::printf("{\"n\": %ld, \"b\": %d, \"N\": %d, \"workers\": %d, \"closure_tiles\": %zu, \"seconds\": %.3f, "
+              "\"logdet\": %.17g, \"trace\": %.17g, \"matrix_checksum\": %llu, \"factor_checksum\": %llu, "
+              "\"result_checksum\": %llu, \"block\": %d, ",
+              n, b, N, workers, sigma.closure.size(), secs(t0, t1), logdet, trace,
+              static_cast<unsigned long long>(msum), static_cast<unsigned long long>(fsum),
+              static_cast<unsigned long long>(payload_checksum(sigma.blocks)), s);
+  print_tiles("sampled", sampled);
+  std::printf("}\n");
+  return 0;
+}
+
 int main(int argc, char** argv) {
   if (argc >= 8 && std::string(argv[1]) == "symbolic") return symbolic_main(argc, argv);
+  // ref_driver golden n w t b seed workers prefix [density]
+  if (argc >= 9 && std::string(argv[1]) == "golden") {
+    const double density = argc > 9 ? std::atof(argv[9]) : 1.0;
+    GeneratedMatrix gen = generate_arrowhead(
+        {std::atol(argv[2]), std::atol(argv[3]), std::atol(argv[4]), density, std::strtoull(argv[6], nullptr, 10)},
+        std::atoi(argv[5]));
+    return golden_run(gen.matrix, std::atoi(argv[7]), argv[8]);
+  }
+  // ref_driver golden_mm file.mtx b workers prefix   (read_matrix_market_file, matgen.cpp:321-327)
+  if (argc >= 6 && std::string(argv[1]) == "golden_mm") {
+    const TiledSymmetricMatrix m = read_matrix_market_file(argv[2], std::atoi(argv[3]));
+    return golden_run(m, std::atoi(argv[4]), argv[5]);
+  }
+  // ref_driver checksum n w t b seed [density]: payload_checksum of the generated matrix
+  if (argc >= 7 && std::string(argv[1]) == "checksum") {
+    const double density = argc > 7 ? std::atof(argv[7]) : 1.0;
+    GeneratedMatrix gen = generate_arrowhead(
+        {std::atol(argv[2]), std::atol(argv[3]), std::atol(argv[4]), density, std::strtoull(argv[6], nullptr, 10)},
+        std::atoi(argv[5]));
+    std::printf("%llu\n", static_cast<unsigned long long>(payload_checksum(gen.matrix.blocks)));
+    return 0;
+  }
   if (argc < 8) {
     std::fprintf(stderr, "usage: ref_driver bench|dump n w t b seed workers [prefix] [density]\n");
     return 2;

@@ -126,6 +126,14 @@ class Matrix:
                                     pay.ctypes.data_as(C.POINTER(C.c_double))))
         return ti, tj, pay
 
+    @property
+    def checksum(self) -> int:
+        """payload_checksum (storage.cpp:34-48) of the tiles: equals the
+        reference's value for the same matrix."""
+        out = C.c_uint64()
+        _check(lib.tib_matrix_checksum(self._h, C.byref(out)))
+        return out.value
+
     def to_dense(self) -> np.ndarray:
         """dense_from_tiled (oracle.cpp:24-45), with the reference's n <= 4000 guard."""
         n, b, N, s = self._info()
@@ -289,10 +297,20 @@ def _new_handle() -> C.c_void_p:
 
 
 def generate(n: int, bandwidth: int, thickness: int, density: float, seed: int = 0,
-             tile_size: int = 32) -> Matrix:
-    """generate_arrowhead (matgen.cpp:59-120), bit-exact values."""
+             tile_size: int = 32, device: int | None = None) -> Matrix:
+    """generate_arrowhead (matgen.cpp:59-120), bit-exact values.
+
+    ``device=k`` (density 1 only): the values are generated on GPU k straight
+    into each sweep's tile store (generate.cu) -- no host payload, no H2D copy;
+    ``tiles()`` / ``checksum`` / ``write_matrix_market`` read them back from
+    the device."""
     h = _new_handle()
-    _check(lib.tib_matrix_generate(n, bandwidth, thickness, float(density), seed, tile_size, C.byref(h)))
+    if device is None:
+        _check(lib.tib_matrix_generate(n, bandwidth, thickness, float(density), seed, tile_size, C.byref(h)))
+    else:
+        if float(density) != 1.0:
+            raise TileinvError("device generation needs density 1 (the draw index is closed-form only there)")
+        _check(lib.tib_matrix_generate_device(n, bandwidth, thickness, seed, tile_size, device, C.byref(h)))
     return Matrix(h.value)
 
 

@@ -263,6 +263,9 @@ static std::shared_ptr<DevPlan> upload_plan(DataflowPlan&& host, int device, cud
   d->device = device;
   d->grid = dataflow_grid(device);
   if (kWorkers * d->grid <= d->host.q0.workers) throw Error(kErrCuda, "persistent grid too small for the critical queue");
+  // test hook: one task of the plan can never become ready, so the sweep
+  // stalls and must end through the executor's watchdog (tests/test_gpu_parity.py)
+  if (env_int("TIB_TEST_STALL", 0) && !d->host.need.empty()) d->host.need.back() += 1;
   d->tasks.upload(d->host.tasks, s);
   d->segs.upload(d->host.segs, s);
   d->deps.upload(d->host.deps, s);
@@ -415,21 +418,15 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
   a.missing = e.sched + 128 + 256;  // (ctl lines, 256 spare ints, then the per-task counts)
   a.chain = P.chain.p;
   a.dedicate = batch <= env_int("TIB_DEDICATE_MAX_BATCH", 4) ? 1 : 0;
-  // eight-warp chains: the chain task is q0 task 0 and initially ready, so q0
-  // items 0 .. batch-1 are the chains; they run on CTAs 0 .. batch-1
-  a.chain8 = (a.dedicate && !P.host.chain.empty() && !P.host.init0.empty() && P.host.init0[0] == 0 &&
-              P.host.tasks[0].kind == kChainTask && batch <= P.grid && env_int("TIB_CHAIN8", 0) != 0)
-                 ? 1
-                 : 0;
-  if (a.chain8) a.dedicate = 0;
   a.static_chains = (!P.host.chain.empty() && !P.host.init0.empty() && P.host.init0[0] == 0 &&
                      P.host.tasks[0].kind == kChainTask && batch <= P.grid)
                         ? 1
                         : 0;
   // the chains' workers are reserved ones (worker 0 of the first CTAs): keep
   // the plan's count of reserved workers for the chain's helpers
-  if (a.static_chains || a.chain8) a.q0.workers += batch;
+  if (a.static_chains) a.q0.workers += batch;
   a.poll_uploads = poll ? 1 : 0;
+  a.watchdog_ns = static_cast<unsigned long long>(env_int("TIB_WATCHDOG_S", 60)) * 1000000000ull;
   a.slots0 = a.missing + nt * batch;
   a.slots1 = a.slots0 + static_cast<size_t>(P.host.q0.count) * batch;
   a.trace = nullptr;
@@ -488,13 +485,84 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
   CK(cudaGraphLaunch(e.exec, s));
 }
 
+// Largest batch one launch may carry: every chain needs its own CTA (static
+// chain assignment, worker 0 of CTA m runs matrix m's chain) and queue items
+// pack (matrix, task) into a non-negative int.  Bigger batches run as several
+// launches of the same plan.
+static size_t max_batch(const DevPlan& P) {
+  const size_t by_items = static_cast<size_t>(INT_MAX) / std::max<size_t>(P.host.tasks.size(), 1);
+  const size_t by_chains = P.host.chain.empty() ? by_items : static_cast<size_t>(P.grid);
+  return std::max<size_t>(1, std::min(by_items, by_chains));
+}
+
+static void run_flow_chunked(DevPlan& P, const std::vector<BaseTable>& tables, cudaStream_t s,
+                             const std::function<void()>* pre_launch = nullptr) {
+  const size_t mb = max_batch(P);
+  if (tables.size() <= mb) {
+    run_flow(P, tables, s, pre_launch);
+    return;
+  }
+  if (pre_launch) throw Error(kErrInvalidArgument, "streamed upload is single-launch only");
+  for (size_t i = 0; i < tables.size(); i += mb) {
+    const std::vector<BaseTable> part(tables.begin() + static_cast<long>(i),
+                                      tables.begin() + static_cast<long>(std::min(tables.size(), i + mb)));
+    run_flow(P, part, s);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // objects behind the handles
 struct MatrixObj {
   Layout layout;
   Pattern pattern;
-  HostBuf payload;  // pattern.size() * b * b, pinned when a device exists
+  mutable HostBuf payload;  // pattern.size() * b * b, pinned when a device exists
+  // device-generated matrix (tib_matrix_generate_device): the values are made
+  // on the device straight into each sweep's A store; the host payload is
+  // materialised (from the device) only when a host-side API asks for it
+  struct DevGen {
+    bool on = false;
+    long n = 0, w = 0, t = 0;
+    uint64_t seed = 0;
+    int device = 0;
+  } gen;
 };
+
+// Generator on the device (generate.cu) into a tile store over `pat` with row
+// stride bp (identity padding), stream-ordered.
+static void device_generate(const MatrixObj& m, const Pattern& pat, int bp, double* out, cudaStream_t s) {
+  std::vector<int> ti(pat.size()), tj(pat.size());
+  for (size_t k = 0; k < pat.size(); ++k) {
+    ti[k] = pat.tiles()[k].i;
+    tj[k] = pat.tiles()[k].j;
+  }
+  int* d_ij = nullptr;
+  double* d_diag = nullptr;
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&d_ij), 2 * pat.size() * sizeof(int), s));
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&d_diag), static_cast<size_t>(m.gen.n) * sizeof(double), s));
+  CK(cudaMemcpyAsync(d_ij, ti.data(), ti.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_ij + pat.size(), tj.data(), tj.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+  CK(static_cast<cudaError_t>(launch_generate_arrowhead(m.gen.n, m.gen.w, m.gen.t, m.gen.seed, m.layout.b, bp, d_ij,
+                                                        d_ij + pat.size(), static_cast<long>(pat.size()), d_diag, out, s)));
+  CK(cudaFreeAsync(d_ij, s));
+  CK(cudaFreeAsync(d_diag, s));
+  CK(cudaStreamSynchronize(s));  // the host vectors above die with this scope
+}
+
+static DeviceRt& runtime(int device);
+
+// Host payload of m (materialised from the device generator on first use).
+static const double* host_payload(const MatrixObj& m) {
+  if (m.gen.on && m.payload.n == 0) {
+    DeviceRt& rt = runtime(m.gen.device);
+    const size_t bb = static_cast<size_t>(m.layout.b) * m.layout.b;
+    DevBuf d(m.pattern.size() * bb, m.gen.device, rt.stream);
+    device_generate(m, m.pattern, m.layout.b, d.p, rt.stream);
+    m.payload.alloc(d.n);
+    CK(cudaMemcpyAsync(m.payload.p, d.p, d.n * sizeof(double), cudaMemcpyDeviceToHost, rt.stream));
+    CK(cudaStreamSynchronize(rt.stream));
+  }
+  return m.payload.p;
+}
 
 struct FactorObj {
   int device = 0;
@@ -525,6 +593,10 @@ static void fill_matrix(MatrixObj& m, HostMatrix&& hm) {
 // identity on the padded diagonal).
 static void upload_matrix(const MatrixObj& m, const Pattern& filled, int bp, double* dA, cudaStream_t s,
                           HostBuf* staging_keep = nullptr) {
+  if (m.gen.on) {  // no host values: generate in place
+    device_generate(m, filled, bp, dA, s);
+    return;
+  }
   const int b = m.layout.b;
   const size_t bb = static_cast<size_t>(b) * b, bpp = static_cast<size_t>(bp) * bp;
   if (bp == b && filled == m.pattern) {
@@ -577,10 +649,22 @@ static void alloc_factor_stores(SweepStores& st, const FactorPlan2& P, int batch
   st.status = DevBuf(static_cast<size_t>(batch), dev, s);
 }
 
+// After a stream sync: a sweep that hit the executor's watchdog (kernels.cu
+// Spin) raises TIB_ERR_CUDA with the dependency it gave up on.
+static void check_watchdog() {
+  int rec[4] = {0, 0, 0, 0};
+  CK(static_cast<cudaError_t>(read_watchdog(rec)));
+  if (rec[0])
+    throw Error(kErrCuda, "dataflow watchdog: a sweep waited longer than TIB_WATCHDOG_S on counter " +
+                              std::to_string(rec[1]) + " >= " + std::to_string(rec[2]) + " (dependency " +
+                              std::to_string(rec[3]) + "); results discarded");
+}
+
 static void check_status(const DevBuf& status, int batch, const Layout& L, cudaStream_t s, int* bad_index = nullptr) {
   std::vector<unsigned long long> h(static_cast<size_t>(batch));
   CK(cudaMemcpyAsync(h.data(), status.p, batch * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  check_watchdog();
   for (int k = 0; k < batch; ++k)
     if (h[static_cast<size_t>(k)] != ULLONG_MAX) {
       const long pivot = static_cast<long>(h[static_cast<size_t>(k)]);
@@ -601,11 +685,11 @@ static double reduce_logdet(const double* parts, int N, int nb) {
 static void factor_sweep(FactorPlan2& P, SweepStores& st, cudaStream_t s, const std::vector<BaseTable>& tables,
                          const std::function<void()>* pre_launch = nullptr) {
   CK(cudaMemsetAsync(st.status.p, 0xff, tables.size() * sizeof(unsigned long long), s));
-  run_flow(*P.flow, tables, s, pre_launch);
+  run_flow_chunked(*P.flow, tables, s, pre_launch);
 }
 
 static void phase2_sweep(Phase2Plan& P, cudaStream_t s, const std::vector<BaseTable>& tables) {
-  run_flow(*P.flow, tables, s);
+  run_flow_chunked(*P.flow, tables, s);
 }
 
 static BaseTable make_table(double* A, double* L, double* P1, double* Sg, double* var, double* scratch,
@@ -649,7 +733,7 @@ static SigmaObj* selected_inverse_matrix(const MatrixObj& m, const Request& req,
   // The A store goes up tile column by tile column on the upload stream while
   // the factor sweep runs (tasks poll each column's counter); only possible
   // when the host payload already has the device layout (b = bp, no fill-in).
-  const bool stream_up = fp->bp == m.layout.b && F == m.pattern && m.payload.pinned &&
+  const bool stream_up = !m.gen.on && fp->bp == m.layout.b && F == m.pattern && m.payload.pinned &&
                          env_int("TIB_STREAM_UPLOAD", 1) != 0 && fp->flow->host.upl >= 0;
   if (!stream_up) upload_matrix(m, F, fp->bp, st.A.p, s);
   auto* res = new SigmaObj;
@@ -832,7 +916,8 @@ int tib_matrix_write_mm(tib_matrix m, char* buf, size_t* len) {
     HostMatrix hm;
     hm.layout = m->layout;
     hm.pattern = m->pattern;
-    hm.payload.assign(m->payload.p, m->payload.p + m->payload.n);
+    const double* pay = host_payload(*m);
+    hm.payload.assign(pay, pay + m->payload.n);
     const std::string text = write_matrix_market(hm);
     if (buf && *len >= text.size()) std::memcpy(buf, text.data(), text.size());
     *len = text.size();
@@ -854,7 +939,31 @@ int tib_matrix_tiles(tib_matrix m, int* ti, int* tj, double* payload) {
       if (ti) ti[k] = m->pattern.tiles()[k].i;
       if (tj) tj[k] = m->pattern.tiles()[k].j;
     }
-    if (payload) std::memcpy(payload, m->payload.p, m->payload.n * sizeof(double));
+    if (payload) {
+      const double* pay = host_payload(*m);
+      std::memcpy(payload, pay, m->payload.n * sizeof(double));
+    }
+  });
+}
+int tib_matrix_generate_device(long n, long w, long t, uint64_t seed, int b, int device, tib_matrix* out) {
+  return guarded([&] {
+    runtime(device);  // no device: TIB_ERR_CUDA (no host fallback for a device matrix)
+    auto* m = new tib_matrix_s;
+    m->pattern = arrowhead_pattern(n, w, t, b);
+    m->layout = m->pattern.layout();
+    m->gen.on = true;
+    m->gen.n = n;
+    m->gen.w = w;
+    m->gen.t = t;
+    m->gen.seed = seed;
+    m->gen.device = device;
+    *out = m;
+  });
+}
+int tib_matrix_checksum(tib_matrix m, uint64_t* out) {
+  return guarded([&] {
+    need(m, "matrix");
+    *out = checksum_store(host_payload(*m), m->pattern, m->layout.b, m->layout.b);
   });
 }
 int tib_matrix_free(tib_matrix m) {
@@ -1000,6 +1109,7 @@ int tib_selected_inverse_of_factor(tib_factor f, int preset, const long* rows, c
     std::vector<BaseTable> tables{make_table(nullptr, f->L.p, f->P1.p, res->S.p, res->var.p, scratch.p, nullptr, nullptr, ctr.p)};
     phase2_sweep(*p2, s, tables);
     CK(cudaStreamSynchronize(s));
+    check_watchdog();
     *out = guard.release();
   });
 }

@@ -35,12 +35,14 @@ struct FlowArgs {
   int* ctl;      // head0, tail0, head1, tail1 (128-byte apart)
   const DTask* chain;  // chain steps (kChainTask)
   int dedicate;        // chains get their SM to themselves
-  int chain8;          // chains run on both workers of CTAs 0 .. batch-1 (q0 items 0 .. batch-1 skipped)
   int static_chains;   // chains run on worker 0 of CTAs 0 .. batch-1 (q0 items 0 .. batch-1 skipped)
   int poll_uploads;    // streamed upload: tasks wait for their A-store column (DTask::poll)
+  unsigned long long watchdog_ns;  // a spin longer than this aborts the sweep (TIB_ERR_CUDA)
   unsigned long long* trace;
 };
 
+// Sticky watchdog record {flag, counter, value, dep index}; cleared once read.
+int read_watchdog(int* rec);
 // Chain phase profile accumulator (16 long longs of device memory) or null.
 int set_chain_profile(long long* p);
 
@@ -48,5 +50,9 @@ void launch_dataflow(const FlowArgs& a, const int* need, const int* init0, int n
                      int grid, cudaStream_t s);
 void launch_zero_strips(const ZeroStrip* z, int count, int ld, int batch, const BaseTable* tables, cudaStream_t s);
 void launch_fill(double* p, double v, size_t count, cudaStream_t s);
+// generate.cu: density-1 arrowhead generator (matgen.cpp:59-120) into a tile
+// store over the given slots (row stride bp); diag_scratch holds n doubles.
+int launch_generate_arrowhead(long n, long w, long t, unsigned long long seed, int b, int bp, const int* slot_ti,
+                              const int* slot_tj, long slots, double* diag_scratch, double* out, cudaStream_t s);
 
 }  // namespace tib

@@ -8,6 +8,7 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <set>
 #include <string>
 
 namespace tib {
@@ -56,6 +57,24 @@ struct Builder {
     ++t.seg_count;
     P.task_flops += 2.0 * kB * kB * (khi - klo);
   }
+  // Appends signal c to task t (its signal list is copied to the end of sigs).
+  void add_sig(DTask& t, int c) {
+    const int nb0 = static_cast<int>(P.sigs.size());
+    for (int s = t.sig_begin; s < t.sig_begin + t.sig_count; ++s) P.sigs.push_back(P.sigs[static_cast<size_t>(s)]);
+    P.sigs.push_back(c);
+    t.sig_begin = nb0;
+    ++t.sig_count;
+  }
+  // Adds a first-phase dependency to task t (its dependency list is copied).
+  void add_dep(DTask& t, Dep d) {
+    const int nb0 = static_cast<int>(P.deps.size());
+    for (int k = t.dep_begin; k < t.dep_begin + t.dep_count; ++k) P.deps.push_back(P.deps[static_cast<size_t>(k)]);
+    P.deps.push_back(d);
+    for (int k = t.dep_begin + t.dep_count; k < t.dep_begin + t.dep_count + t.dep2_count; ++k)
+      P.deps.push_back(P.deps[static_cast<size_t>(k)]);
+    t.dep_begin = nb0;
+    ++t.dep_count;
+  }
   // Splits the emission order into the two queues; returns the global order
   // expressed in final task indices.
   std::vector<int> finish(int crit_workers, bool chain = false) {
@@ -94,6 +113,18 @@ struct Builder {
       }
       all.insert(all.end(), rest.begin(), rest.end());
       queue.insert(queue.end(), rq.begin(), rq.end());
+      // a boundary leaf may carry its block to the next step only if that step
+      // is the block's leaf and no other column updates the block in between
+      // (the leaf's dependency value is the count this step's signal reaches)
+      for (size_t s = 0; s + 1 < P.chain.size(); ++s) {
+        DTask& c0 = P.chain[s];
+        const DTask& c1 = P.chain[s + 1];
+        if (!(c0.mode & 4) || c1.dep_count < 1) continue;
+        const Seg& sx = P.segs[static_cast<size_t>(c0.seg_begin)];
+        const Dep& d = P.deps[static_cast<size_t>(c1.dep_begin)];
+        const int aord_sig = P.sigs[static_cast<size_t>(c0.sig_begin + c0.sig_count - 2)];
+        if (c1.c_off == sx.b_off && d.counter == aord_sig && d.value == c0.aux0) c0.mode |= kCarry;
+      }
     }
     std::vector<int> pos(all.size());
     P.tasks.clear();
@@ -110,10 +141,6 @@ struct Builder {
         P.tasks.push_back(all[i]);
       }
     P.q0 = QueueDesc{0, n0, n0 > 0 ? crit_workers : 0, 0};
-    if (chain)  // chain steps reference tasks by emission index: to final indices
-      for (DTask& s : P.chain)
-        for (int* f : {&s.aux0, &s.aux1, &s.pad2})
-          if (*f >= 0) *f = pos[static_cast<size_t>(conv[static_cast<size_t>(*f)])];
     P.q1 = QueueDesc{n0, static_cast<int>(P.tasks.size()) - n0, 0, 0};
     finalize_waiters();
     return pos;
@@ -232,7 +259,7 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
              cXblk = cLfin + T, cXfin = cXblk + static_cast<long>(N) * NB2, cTblk = cXfin + N,
              cWfin = cTblk + static_cast<long>(N) * NB2, cXrow = cWfin + T, cArrive = cXrow + static_cast<long>(N) * nb,
              cSdone = cArrive + static_cast<long>(N) * slots_per_col, cUpl = cSdone + static_cast<long>(N) * NB2,
-             cMdone = cUpl + N, cEnd = cMdone + static_cast<long>(N) * nb;
+             cMdone = cUpl + N, cClip = cMdone + static_cast<long>(N) * nb, cRing = cClip + N, cEnd = cRing + N;
   P.upl = cUpl;
   P.counters = cEnd;
   const size_t t_doubles = static_cast<size_t>(N) * bp * bp;
@@ -249,6 +276,14 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
   auto xrowc = [&](int j, int q) { return static_cast<int>(cXrow + static_cast<long>(j) * nb + q); };
   auto sdone = [&](int j, int q, int p) { return static_cast<int>(cSdone + static_cast<long>(j) * NB2 + q * nb + p); };
   auto mdone = [&](int j, int q) { return static_cast<int>(cMdone + static_cast<long>(j) * nb + q); };
+  // clipped part of column j's update of block (0, 0) of tile (k0, k0) done
+  // (the boundary leaf applies the last term and is the block's one update signal)
+  auto clipdone = [&](int j) { return static_cast<int>(cClip + j); };
+  // ring release: split groups (and the boundary leaf) of column j finished with
+  // the column's scratch ring slots
+  auto ringdone = [&](int j) { return static_cast<int>(cRing + j); };
+  // ring slot of column j (columns kRing apart share one)
+  auto ring_of = [&](int j) { return static_cast<long long>(j % kRing); };
   const int xdone = nb * (nb + 1) / 2;
   const long long tsz = static_cast<long long>(bp) * bp;
 
@@ -274,7 +309,9 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
     }
   };
 
+  std::vector<int> ring_count(static_cast<size_t>(N), 0);
   for (int j = 0; j < N; ++j) {
+    const size_t col_first = B.all.size();
     const long ds = F.col_start(j);
     const int U = ord[static_cast<size_t>(ds)];
     const int valid = static_cast<int>(std::min<long>(L.b, L.n - static_cast<long>(j) * L.b));
@@ -297,13 +334,13 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
     const bool bnd_col = bnd && tail0;
     auto s_off = [&](int q, int p) {  // reduced S^q_p block of this column (ring slot)
       return static_cast<long long>(t_doubles) +
-             (static_cast<long long>(j % kRing) * slots_per_col + 2 * panel_slots + 2 * upd_slots +
+             (ring_of(j) * slots_per_col + 2 * panel_slots + 2 * upd_slots +
               sq_out_base[static_cast<size_t>(q)] + p) *
                  kB * kB;
     };
     auto m_off = [&](int q) {  // M_q of this column (ring slot)
       return static_cast<long long>(t_doubles) +
-             (static_cast<long long>(j % kRing) * slots_per_col + 2 * panel_slots + 2 * upd_slots + s_slots + q) * kB * kB;
+             (ring_of(j) * slots_per_col + 2 * panel_slots + 2 * upd_slots + s_slots + q) * kB * kB;
     };
     // ---- diagonal-tile chain (queue 0): blocked POTRF + TRTRI of tile (j, j)
     // Fat leaf: factor + invert block (kk, kk), then (kk + 1 < nb, after the
@@ -327,15 +364,20 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
       } else if (bleaf) {
         d2.push_back({sdone(j, nb - 1, 0), 1});
         d2.push_back({afin(sk0), Uk0 * NB2});
-        d2.push_back({aord(ts00, 0, 0), u00 + 1});
+        d2.push_back({clipdone(j), 1});
         sg.push_back(lblk(sk0, 0, nb - 1));
         sg.push_back(lfin(sk0));
         sg.push_back(aord(ts00, 0, 0));
+        sg.push_back(ringdone(j));
       }
       DTask& t = B.add(0, d, sg, d2);
-      t.sig2_count = (fat || bleaf) ? 3 : 0;
+      t.sig2_count = fat ? 3 : (bleaf ? 4 : 0);
       t.kind = kLeafTask;
-      t.mode = fat ? 2 : (bleaf ? 4 : 0);
+      // kCarry: the chain may keep the block this step updates last (the next
+      // diagonal block) in shared memory for its next step -- always within a
+      // tile; for a boundary leaf decided once the consumer is known (finish)
+      t.mode = fat ? (2 | kCarry) : (bleaf ? 4 : 0);
+      if (bleaf) t.aux0 = u00 + 1;  // block (0, 0) update count after this leaf
       if (bleaf) {
         t.p_off = blk_off(sk0, bp, 0, nb - 1);  // P in the A store; L(k0, j)[0, nb-1] at the same offset in L
         Seg sgx{};
@@ -419,7 +461,7 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
           if (parts > 1) {
             const int slot = base + p * parts;
             t.p_off = static_cast<long long>(t_doubles) +
-                      (static_cast<long long>(j % kRing) * slots_per_col + slot) * kB * kB;
+                      (ring_of(j) * slots_per_col + slot) * kB * kB;
             t.aux0 = static_cast<int>(cArrive + static_cast<long>(j) * slots_per_col + slot);
             t.aux1 = (r << 8) | parts;
           }
@@ -454,6 +496,7 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
           if (parts == 1) d.insert(d.end(), d2.begin(), d2.end());
           std::vector<int> sg{aord(ts, p, q)};
           if (a != c) sg.push_back(afin(ts));
+          if (clip) sg = {clipdone(j)};
           DTask& t = B.add(queue, d, sg, parts > 1 ? d2 : std::vector<Dep>{});
           t.kind = parts > 1 ? kSplitTask : kGemmTask;
           t.c_store = t.c0_store = kStoreA;
@@ -465,7 +508,7 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
             // so their slots are addressed by block index
             const int slot = slot_base + (p * nb + q) * upd_parts;
             t.p_off = static_cast<long long>(t_doubles) +
-                      (static_cast<long long>(j % kRing) * slots_per_col + slot) * kB * kB;
+                      (ring_of(j) * slots_per_col + slot) * kB * kB;
             t.aux0 = static_cast<int>(cArrive + static_cast<long>(j) * slots_per_col + slot);
             t.aux1 = (r << 8) | parts;
             if (parts == 1) t.kind = kGemmTask;
@@ -503,7 +546,7 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
           if (sp > 1) {
             const int slot = 2 * panel_slots + 2 * upd_slots + sq_part_base[static_cast<size_t>(q)] + p * s_parts(q);
             t.p_off = static_cast<long long>(t_doubles) +
-                      (static_cast<long long>(j % kRing) * slots_per_col + slot) * kB * kB;
+                      (ring_of(j) * slots_per_col + slot) * kB * kB;
             t.aux0 = static_cast<int>(cArrive + static_cast<long>(j) * slots_per_col + slot);
             t.aux1 = (r << 8) | sp;
           }
@@ -556,7 +599,7 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
           t.c_store = kStoreL;
           t.c_off = blk_off(sk0, bp, p, q);
           t.p_off = static_cast<long long>(t_doubles) +
-                    (static_cast<long long>(j % kRing) * slots_per_col + slot) * kB * kB;
+                    (ring_of(j) * slots_per_col + slot) * kB * kB;
           t.aux0 = static_cast<int>(cArrive + static_cast<long>(j) * slots_per_col + slot);
           t.aux1 = (r << 8) | 2;
           return t;
@@ -571,40 +614,17 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
       }
     };
     for (int kk = 0; kk < nb; ++kk) {
-      const int li = static_cast<int>(B.all.size());
       leaf(kk);
-      if (chain && kk >= 1 && kk + 1 < nb) B.all[static_cast<size_t>(li)].mode |= 8;
       if (kk + 1 < nb && !fat_leaf) {
         paneld(kk + 1, kk);
         traild(kk + 1, kk + 1, kk);
       }
       for (int k = 0; k < kk; ++k) xrow(kk, k);
       for (int k = 0; k <= kk && kk + 1 < nb; ++k) tterm(kk + 1, k, kk);
-      // chain lookahead (eight-warp chain): the panel block L(kk+2, kk) and
-      // its kk terms on blocks (kk+2, kk+1) and (kk+2, kk+2) -- the next
-      // step's second-phase operands -- are formed by the chain itself; the
-      // tasks stay in the plan for the other executors, marked chain-owned
-      // (pad2) and referenced from the step (aux0, aux1, pad2: emission index)
-      int la[3] = {-1, -1, -1};
-      for (int i = kk + 2; i < nb; ++i) {
-        if (chain && i == kk + 2) la[0] = static_cast<int>(B.all.size());
-        paneld(i, kk);
-      }
+      for (int i = kk + 2; i < nb; ++i) paneld(i, kk);
       for (int p = kk + 1; p < nb; ++p)
         for (int i = p; i < nb; ++i)
-          if (!(i == kk + 1 && p == kk + 1)) {
-            if (chain && i == kk + 2 && p == kk + 1) la[1] = static_cast<int>(B.all.size());
-            if (chain && i == kk + 2 && p == kk + 2) la[2] = static_cast<int>(B.all.size());
-            traild(i, p, kk);
-          }
-      {
-        DTask& lt = B.all[static_cast<size_t>(li)];
-        lt.aux0 = la[0];
-        lt.aux1 = la[1];
-        lt.pad2 = la[2];
-        for (int x : la)
-          if (x >= 0) B.all[static_cast<size_t>(x)].pad2 = 1;
-      }
+          if (!(i == kk + 1 && p == kk + 1)) traild(i, p, kk);
       for (int kk2 = kk + 2; kk2 < nb; ++kk2)
         for (int k = 0; k <= kk; ++k) tterm(kk2, k, kk);
       if (tail0 && !bnd_col) {
@@ -679,6 +699,29 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
     for (size_t ia = 2; ia < krows.size(); ++ia) update(ia, 0);
     for (size_t ic = 1; ic < krows.size(); ++ic)
       for (size_t ia = ic; ia < krows.size(); ++ia) update(ia, ic);
+    // scratch ring: every split group of column j (and its boundary leaf, which
+    // reads S_0) signals ringdone(j) when done with the column's ring slots;
+    // the ring writers of column j wait for the column that used the same
+    // slots before (kRing columns earlier) to be done with them -- implied by
+    // the data dependencies on band patterns, required for any other
+    {
+      std::set<int> groups;  // arrival counters (parts of one group are not contiguous)
+      for (size_t x = col_first; x < B.all.size(); ++x) {
+        DTask& t = B.all[x];
+        if (t.kind != kSplitTask) continue;
+        groups.insert(t.aux0);
+        B.add_sig(t, ringdone(j));
+      }
+      ring_count[static_cast<size_t>(j)] = static_cast<int>(groups.size()) + (bnd_col ? 1 : 0);
+      const int prev = j - kRing;
+      if (prev >= 0 && ring_count[static_cast<size_t>(prev)] > 0)
+        for (size_t x = col_first; x < B.all.size(); ++x) {
+          DTask& t = B.all[x];
+          const bool writer = t.kind == kSplitTask || (t.kind == kGemmTask && t.c_store == kStoreScratch &&
+                                                        t.c_off >= static_cast<long long>(t_doubles));
+          if (writer) B.add_dep(t, {ringdone(prev), ring_count[static_cast<size_t>(prev)]});
+        }
+    }
     if (j - defer_w >= 0) emit_w(j - defer_w);
   }
   for (int j = std::max(0, N - defer_w); j < N; ++j) emit_w(j);

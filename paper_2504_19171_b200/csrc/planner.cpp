@@ -264,6 +264,31 @@ struct SplitMix64 {
 // over the same SplitMix64 stream: the first decides which tiles receive an
 // entry (with density < 1 a band tile may stay empty), the second writes
 // values straight into the packed slot-ordered payload.
+// Tile pattern of generate_arrowhead at density 1 (every band slot accepted):
+// the touched tiles follow from the index ranges alone.
+Pattern arrowhead_pattern(long n, long w, long t, int b) {
+  if (n < 1) throw Error(kErrInvalidArgument, "generator: n must be positive");
+  if (t < 0 || t >= n) throw Error(kErrInvalidArgument, "generator: thickness must satisfy 0 <= t < n");
+  if (w < 0 || w >= n - t) throw Error(kErrInvalidArgument, "generator: bandwidth must satisfy 0 <= w < n - t");
+  const Layout L = build_layout(n, b);
+  std::vector<std::vector<char>> touched(static_cast<size_t>(L.N));
+  for (int j = 0; j < L.N; ++j) touched[static_cast<size_t>(j)].assign(static_cast<size_t>(L.N - j), 0);
+  for (long r = 0; r < n; ++r) {
+    const int ti = static_cast<int>(r / b);
+    const long c0 = r < n - t ? std::max(0l, r - w) : 0;
+    if (c0 >= r) continue;
+    for (int tj = static_cast<int>(c0 / b); tj <= static_cast<int>((r - 1) / b); ++tj)
+      touched[static_cast<size_t>(tj)][static_cast<size_t>(ti - tj)] = 1;
+  }
+  std::vector<Coord> tiles;
+  for (int j = 0; j < L.N; ++j) {
+    touched[static_cast<size_t>(j)][0] = 1;
+    for (int d = 0; d < L.N - j; ++d)
+      if (touched[static_cast<size_t>(j)][static_cast<size_t>(d)]) tiles.push_back({j + d, j});
+  }
+  return Pattern(L, std::move(tiles));
+}
+
 HostMatrix generate_arrowhead(long n, long w, long t, double density, uint64_t seed, int b) {
   if (n < 1) throw Error(kErrInvalidArgument, "generator: n must be positive");
   if (t < 0 || t >= n) throw Error(kErrInvalidArgument, "generator: thickness must satisfy 0 <= t < n");

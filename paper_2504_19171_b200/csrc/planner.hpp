@@ -188,6 +188,8 @@ struct HostMatrix {
 
 // Bit-exact restatement of generate_arrowhead (proj/src/matgen.cpp:59-120).
 HostMatrix generate_arrowhead(long n, long w, long t, double density, uint64_t seed, int b);
+// Its tile pattern at density 1 (no values; the device generator fills them).
+Pattern arrowhead_pattern(long n, long w, long t, int b);
 HostMatrix matrix_from_dense(long n, int b, const double* a);  // module.cpp:46-74
 HostMatrix matrix_from_tiles(long n, int b, long count, const int* ti, const int* tj,
                              const double* payload);

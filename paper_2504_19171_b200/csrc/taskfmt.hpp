@@ -56,6 +56,11 @@ struct Task {
   unsigned char diag_store, pad0, pad1, pad2;
 };
 
+// Leaf / chain-step mode bits (DTask::mode of a kLeafTask): 1 invert only,
+// 2 fat leaf, 4 tile-boundary leaf, kCarry: the block the step updates last
+// is the next chain step's, which may take it from shared memory.
+constexpr int kCarry = 16;
+
 enum TaskKind : unsigned char { kGemmTask = 0, kLeafTask = 1, kSplitTask = 2, kChainTask = 3 };
 
 // One schedulable unit of a sweep.  kGemmTask: C / C0 / Cm / diag stores and

@@ -13,6 +13,15 @@ this; it only reads the committed fixtures.
                   column work lists (ref_driver symbolic) per case
   small.npz       diag(Sigma), logdet, trace of the SURVEY small config
                   (n=10000 w=200 t=50 b=128 seed 42) from ref_driver dump
+  config_*.npz    BASELINE configs 2, 3, 5 (medium, large, batch members 1000
+                  and 1063) from `ref_driver golden` (the reference's own
+                  factorize + phase1 + phase2, 8 workers): diag(Sigma), logdet,
+                  trace, payload_checksum of the generated matrix, per closure
+                  tile (Frobenius norm, sum, weighted sum), and the leading /
+                  trailing 64 x 64 blocks of sampled tiles (last three tile
+                  columns, the middle column, arrow tiles).  Large takes ~4 min.
+    python tests/golden/make_golden.py configs [DIR]   (DIR: reuse outputs of
+    an earlier `ref_driver golden` run written as DIR/<name>.*)
 """
 import json
 import os
@@ -50,7 +59,52 @@ def sel_arg(sel):
     return ";".join(f"{r},{c}" for r, c in sel)
 
 
+CONFIGS = {
+    # name: n, w, t, b, seed
+    "medium": (100000, 1000, 100, 256, 42),
+    "large": (200000, 2000, 200, 512, 42),
+    "batch1000": (50000, 500, 50, 128, 1000),
+    "batch1063": (50000, 500, 50, 128, 1063),
+}
+
+
+def pack_config(name, prefix, info, args):
+    n, w, t, b, seed = args
+    s = info["block"]
+    sampled = np.array(info["sampled"], dtype=np.int32).reshape(-1, 2)
+    np.savez_compressed(
+        os.path.join(HERE, f"config_{name}.npz"),
+        args=np.array(args, dtype=np.int64),
+        diag=np.fromfile(prefix + ".diag.f64", dtype=np.float64),
+        tstats=np.fromfile(prefix + ".tstats.f64", dtype=np.float64).reshape(-1, 3),
+        blocks=np.fromfile(prefix + ".blocks.f64", dtype=np.float64).reshape(len(sampled), 2, s, s),
+        sampled=sampled,
+        logdet=info["logdet"], trace=info["trace"],
+        matrix_checksum=np.uint64(info["matrix_checksum"]),
+        closure_tiles=info["closure_tiles"])
+
+
+def configs(from_dir=None):
+    with tempfile.TemporaryDirectory() as tmp:
+        for name, args in CONFIGS.items():
+            n, w, t, b, seed = args
+            if from_dir:
+                prefix = os.path.join(from_dir, name)
+                info = json.load(open(prefix + ".json"))
+            else:
+                prefix = os.path.join(tmp, name)
+                out = subprocess.run([os.path.join(REF, "ref_driver"), "golden", str(n), str(w), str(t), str(b),
+                                      str(seed), str(os.cpu_count()), prefix],
+                                     check=True, capture_output=True, text=True).stdout
+                info = json.loads(out)
+            pack_config(name, prefix, info, args)
+            print("config", name, "logdet", info["logdet"])
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "configs":
+        configs(sys.argv[2] if len(sys.argv) > 2 else None)
+        return
     kat = {}
     a = np.array([[4.0, 2.0], [2.0, 5.0]])
     kat["two_by_two_all"] = R.selected_inverse(R.from_dense(a), "all").entries()

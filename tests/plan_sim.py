@@ -145,8 +145,48 @@ class Sim:
             np.add.at(self.cnt, sg, 1)
 
 
-def run_plans(tib, matrix, selection):
-    """Runs factor + phase-2 plans of `matrix` on the CPU interpreter; returns
+    def run_random(self, seed):
+        """Executes the tasks one at a time in a random order among those whose
+        dependencies (both phases) are met -- the GPU may run any ready task at
+        any time, so a dependency missing from the plan shows up as a wrong
+        result here for some seed."""
+        rng = np.random.default_rng(seed)
+        tasks = self.p["tasks"]
+        deps = self.p["deps"]
+        waiters = {}
+        missing = np.zeros(len(tasks), np.int64)
+        for ti, t in enumerate(tasks):
+            d = deps[t["dep_begin"]:t["dep_begin"] + t["dep_count"] + t["dep2_count"]]
+            for c, v in zip(d["counter"].tolist(), d["value"].tolist()):
+                if v > self.cnt[c]:
+                    missing[ti] += 1
+                    waiters.setdefault((c, v), []).append(ti)
+        ready = [ti for ti in range(len(tasks)) if missing[ti] == 0]
+        done = 0
+        while ready:
+            k = int(rng.integers(len(ready)))
+            ti = ready[k]
+            ready[k] = ready[-1]
+            ready.pop()
+            done += 1
+            t = tasks[ti]
+            if t["kind"] == 1:
+                self.leaf(t)
+            elif not self.gemm(t):
+                continue
+            for c in self.p["sigs"][t["sig_begin"]:t["sig_begin"] + t["sig_count"]].tolist():
+                self.cnt[c] += 1
+                for w in waiters.pop((c, int(self.cnt[c])), []):
+                    missing[w] -= 1
+                    if missing[w] == 0:
+                        ready.append(w)
+        if done != len(tasks):
+            raise RuntimeError(f"dataflow deadlock: {done} of {len(tasks)} tasks ran")
+
+
+def run_plans(tib, matrix, selection, order=None):
+    """Runs factor + phase-2 plans of `matrix` on the CPU interpreter (in-order
+    queue claiming, or a random ready order seeded by `order`); returns
     (factor tiles, closure tiles, Sigma payload [T, b, b], logdet, first bad pivot)."""
     fpat = tib.factor_pattern(matrix)
     closure, _ = tib.closure_tiles(matrix, selection)
@@ -173,8 +213,12 @@ def run_plans(tib, matrix, selection):
         6: np.zeros(N * nb),
     }
     status = [np.iinfo(np.int64).max]
-    Sim(pf, stores, status).run()
-    Sim(pp, stores, status).run()
+    for plan in (pf, pp):
+        sim = Sim(plan, stores, status)
+        if order is None:
+            sim.run()
+        else:
+            sim.run_random(order)
     sig = stores[3].reshape(len(closure), bp, bp)[:, :b, :b]
     logdet = 2.0 * stores[6].sum()
     return fpat, closure, sig, logdet, status[0], stores[4].reshape(N, bp)[:, :b].reshape(-1)[:n]

@@ -20,6 +20,7 @@ CASES = [
     (300, 40, 7, 1.0, 3, 32, [(299, 0), (150, 3), (5, 5), (200, 100)]),
     (400, 0, 30, 1.0, 4, 64, "pattern"),       # no band: diagonal + arrow only
     (1100, 300, 40, 1.0, 9, 256, "pattern"),   # bp = 256: 4x4 blocks per tile
+    (1000, 0, 100, 1.0, 4, 100, "pattern"),    # arrow only, t >= b: first off-diagonal tile is not j + 1
 ]
 
 
@@ -62,3 +63,54 @@ def test_plans_are_topological_for_every_selection(tib):
         for which in (0, 1):
             p = tib.plan_export(m, sel, which, crit_workers=8)
             assert len(p["tasks"]) > 0 and p["q0"] > 0
+
+
+def gapped_arrow(n=900, blocks=(0, 300, 520, 760), t=70, seed=3):
+    """Block-diagonal SPD blocks plus a dense arrow: a tile pattern with gaps
+    below the diagonal (first off-diagonal tile of a column != j + 1)."""
+    rng = np.random.default_rng(seed)
+    a = np.zeros((n, n))
+    edges = list(blocks) + [n - t]
+    for lo, hi in zip(edges[:-1], edges[1:]):
+        m = rng.uniform(-1, 1, (hi - lo, hi - lo))
+        a[lo:hi, lo:hi] = (m + m.T) / 2
+    a[n - t:, :] = rng.uniform(-1, 1, (t, n))
+    a[:, n - t:] = a[n - t:, :].T
+    a = (a + a.T) / 2
+    a[np.diag_indices(n)] = np.abs(a).sum(1) + 1.0
+    return a
+
+
+def test_plan_simulation_gapped_pattern(tib):
+    a = gapped_arrow()
+    m = tib.from_dense(a, tile_size=128)
+    _, closure, sig, logdet, _, var = run_plans(tib, m, "pattern")
+    inv = np.linalg.inv(a)
+    assert abs(logdet - np.linalg.slogdet(a)[1]) <= 1e-12 * abs(logdet)
+    assert normwise(var, np.diag(inv)) <= 1e-12
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+@pytest.mark.parametrize("case", [
+    (700, 90, 12, 1.0, 5, 64, "pattern"),
+    (520, 150, 20, 1.0, 11, 128, "pattern"),
+    (1000, 0, 100, 1.0, 4, 100, "pattern"),
+    (1100, 300, 40, 1.0, 9, 256, "pattern"),
+], ids=lambda c: str(c[:6]) if isinstance(c, tuple) else str(c))
+def test_plan_simulation_random_order(tib, orc, case, seed):
+    """Any ready task may run at any time on the GPU: a random ready order
+    must give the same result (catches dependencies missing from the plan)."""
+    n, w, t, d, s, b, sel = case
+    m = tib.generate(n, w, t, d, seed=s, tile_size=b)
+    _, closure, sig, logdet, _, var = run_plans(tib, m, sel, order=seed)
+    ref = orc.selected_inverse_generated(n, w, t, d, s, b, sel)
+    assert normwise(sig, ref["payload"]) <= 1e-12
+    assert abs(logdet - ref["logdet"]) <= 1e-12 * abs(ref["logdet"])
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_plan_simulation_gapped_random(tib, seed):
+    a = gapped_arrow()
+    m = tib.from_dense(a, tile_size=128)
+    _, closure, sig, logdet, _, var = run_plans(tib, m, "pattern", order=seed)
+    assert normwise(var, np.diag(np.linalg.inv(a))) <= 1e-12
