@@ -64,6 +64,14 @@ int tib_matrix_generate(long n, long bandwidth, long thickness, double density, 
  * materialise the values from the device on first use.                      */
 int tib_matrix_generate_device(long n, long bandwidth, long thickness, uint64_t seed, int tile_size, int device,
                                tib_matrix* out);
+/* BASELINE config 4 (not generable by the reference, which reads it as Matrix
+ * Market, matgen.cpp:321-327): joint INLA precision of an AR1(rho) in time
+ * (nt steps) x SPDE (alpha = 2, K = kappa2 I + lattice Laplacian, Q_s =
+ * tau^2 K^2) on an nx x ny lattice latent field, time-major, plus p fixed
+ * effects (prior precision q_beta, Gaussian likelihood precision tau_y,
+ * covariates from SplitMix64 draws of `seed`) as the dense arrow.           */
+int tib_matrix_generate_kronecker(int nt, int nx, int ny, int p, double rho, double kappa2, double tau,
+                                  double tau_y, double q_beta, uint64_t seed, int tile_size, tib_matrix* out);
 /* payload_checksum (storage.cpp:34-48) of the matrix tiles: FNV-1a over the
  * column-major tile keys and b*b payloads, equal to the reference's value
  * for the same matrix.                                                       */

@@ -9,6 +9,11 @@
 //
 //   ref_driver bench  n w t b seed workers [density]
 //       -> one JSON line {factorize_s, phase1_s, phase2_s, total_s, gflop, ...}
+//   ref_driver bench_mm file.mtx b workers   (the same for a Matrix Market input)
+//   ref_driver golden n w t b seed workers prefix [density]
+//   ref_driver golden_mm file.mtx b workers prefix
+//       -> golden summary files (see golden_run) and a JSON line
+//   ref_driver checksum n w t b seed [density]  -> payload_checksum of the matrix
 //   ref_driver dump   n w t b seed workers out_prefix [density]
 //   ref_driver symbolic n w t b seed density selection
 //       -> {"factor": [[i,j],...], "closure": [[i,j],...], "requested": [...],
@@ -126,7 +131,8 @@ static int symbolic_main(int argc, char** argv) {
 //   <prefix>.tstats.f64  per closure tile (column-major): Frobenius norm, sum,
 //                        weighted sum with w(r, c) = ((7 r + 13 c) mod 11) - 5
 //   <prefix>.blocks.f64  for each sampled tile: the leading s x s block and the
-//                        trailing s x s block of its valid region (s = min(64, b))
+//                        trailing s x s block of its valid region (s = min(64, b);
+//                        starting at row / column max(0, valid - s))
 //   stdout               JSON: logdet, trace, checksums, sampled tile list
 static int golden_run(const TiledSymmetricMatrix& m, int workers, const std::string& prefix) {
   const long n = m.layout.n;
@@ -179,7 +185,7 @@ static int golden_run(const TiledSymmetricMatrix& m, int workers, const std::str
     const auto& p = sigma.blocks.at(tc.i, tc.j);
     const long vr = std::min<long>(b, n - static_cast<long>(tc.i) * b), vc = std::min<long>(b, n - static_cast<long>(tc.j) * b);
     for (int part = 0; part < 2; ++part) {
-      const long r0 = part ? vr - s : 0, c0 = part ? vc - s : 0;
+      const long r0 = part ? std::max(0l, vr - s) : 0, c0 = part ? std::max(0l, vc - s) : 0;
       for (long r = r0; r < r0 + s; ++r)
         bl.write(reinterpret_cast<const char*>(p.data() + r * b + c0), static_cast<std::streamsize>(s * sizeof(double)));
     }
@@ -199,8 +205,38 @@ static int golden_run(const TiledSymmetricMatrix& m, int workers, const std::str
   return 0;
 }
 
+// ref_driver bench_mm file.mtx b workers: the bench timing of a Matrix Market
+// input (read_matrix_market_file, matgen.cpp:321-327; read time excluded).
+static int bench_mm(const std::string& path, int b, int workers) {
+  const auto g0 = Clock::now();
+  const TiledSymmetricMatrix m = read_matrix_market_file(path, b);
+  const auto g1 = Clock::now();
+  const auto t0 = Clock::now();
+  const FactorPlan plan = symbolic_cholesky(m.pattern);
+  TiledFactor factor = factorize(m, plan, workers);
+  const auto t1 = Clock::now();
+  const SelectedTileSet sel =
+      symbolic_inversion(select_tiles(factor.layout, factor.pattern, SelectionRequest::factor_pattern()),
+                         factor.pattern);
+  const auto t2 = Clock::now();
+  factor = phase1(std::move(factor), workers);
+  const auto t3 = Clock::now();
+  SelectedInverse sigma = phase2(factor, sel, workers);
+  const auto t4 = Clock::now();
+  const Flops fl = count_flops(plan, sel, factor.pattern);
+  const double total = secs(t0, t1) + secs(t2, t3) + secs(t3, t4);
+  const double gflop = (fl.fact + fl.p1 + fl.p2) / 1e9;
+  std::printf("{\"n\": %ld, \"b\": %d, \"workers\": %d, \"N\": %d, \"tiles\": %zu, \"read_s\": %.6f, "
+              "\"factorize_s\": %.6f, \"phase1_s\": %.6f, \"phase2_s\": %.6f, \"total_s\": %.6f, "
+              "\"gflop\": %.6f, \"gflops\": %.4f, \"closure_tiles\": %zu}\n",
+              m.layout.n, b, workers, m.layout.N, factor.pattern.size(), secs(g0, g1), secs(t0, t1), secs(t2, t3),
+              secs(t3, t4), total, gflop, gflop / total, sigma.closure.size());
+  return 0;
+}
+
 int main(int argc, char** argv) {
   if (argc >= 8 && std::string(argv[1]) == "symbolic") return symbolic_main(argc, argv);
+  if (argc >= 5 && std::string(argv[1]) == "bench_mm") return bench_mm(argv[2], std::atoi(argv[3]), std::atoi(argv[4]));
   // ref_driver golden n w t b seed workers prefix [density]
   if (argc >= 9 && std::string(argv[1]) == "golden") {
     const double density = argc > 9 ? std::atof(argv[9]) : 1.0;

@@ -314,6 +314,22 @@ def generate(n: int, bandwidth: int, thickness: int, density: float, seed: int =
     return Matrix(h.value)
 
 
+# BASELINE config 4: 50 time steps x 4000 sites (80 x 50 lattice) + 20 fixed effects
+KRONECKER_CONFIG = dict(nt=50, nx=80, ny=50, p=20, rho=0.9, kappa2=0.5, tau=1.0, tau_y=1.0, q_beta=0.01, seed=42)
+
+
+def generate_kronecker(nt: int, nx: int, ny: int, p: int, rho: float = 0.9, kappa2: float = 0.5, tau: float = 1.0,
+                       tau_y: float = 1.0, q_beta: float = 0.01, seed: int = 42, tile_size: int = 32) -> Matrix:
+    """Spatio-temporal Kronecker arrowhead (BASELINE config 4; kronecker.cpp):
+    joint precision of an AR1(rho) x SPDE(nx x ny lattice) latent field (time
+    major) and p fixed effects, the dense arrow.  The reference cannot generate
+    it; it reads it through Matrix Market (``write_matrix_market``)."""
+    h = _new_handle()
+    _check(lib.tib_matrix_generate_kronecker(nt, nx, ny, p, float(rho), float(kappa2), float(tau), float(tau_y),
+                                             float(q_beta), seed, tile_size, C.byref(h)))
+    return Matrix(h.value)
+
+
 def from_dense(array, tile_size: int = 32) -> Matrix:
     a = np.ascontiguousarray(array, dtype=np.float64)
     if a.ndim != 2 or a.shape[0] != a.shape[1]:

@@ -39,6 +39,7 @@ SIGNATURES = {
     "tib_matrix_generate": [_l, _l, _l, _d, C.c_uint64, _i, _pp],
     "tib_matrix_generate_device": [_l, _l, _l, C.c_uint64, _i, _i, _pp],
     "tib_matrix_checksum": [_p, _pu64],
+    "tib_matrix_generate_kronecker": [_i, _i, _i, _i, _d, _d, _d, _d, _d, C.c_uint64, _i, _pp],
     "tib_matrix_from_dense": [_l, _i, _pd, _pp],
     "tib_matrix_from_tiles": [_l, _i, _l, _pi, _pi, _pd, _pp],
     "tib_matrix_read_mm": [C.c_char_p, C.c_size_t, _i, _pp],

@@ -945,6 +945,10 @@ int tib_matrix_tiles(tib_matrix m, int* ti, int* tj, double* payload) {
     }
   });
 }
+int tib_matrix_generate_kronecker(int nt, int nx, int ny, int p, double rho, double kappa2, double tau,
+                                  double tau_y, double q_beta, uint64_t seed, int b, tib_matrix* out) {
+  return guarded([&] { *out = wrap(generate_kronecker(nt, nx, ny, p, rho, kappa2, tau, tau_y, q_beta, seed, b)); });
+}
 int tib_matrix_generate_device(long n, long w, long t, uint64_t seed, int b, int device, tib_matrix* out) {
   return guarded([&] {
     runtime(device);  // no device: TIB_ERR_CUDA (no host fallback for a device matrix)

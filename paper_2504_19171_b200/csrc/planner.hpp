@@ -190,6 +190,10 @@ struct HostMatrix {
 HostMatrix generate_arrowhead(long n, long w, long t, double density, uint64_t seed, int b);
 // Its tile pattern at density 1 (no values; the device generator fills them).
 Pattern arrowhead_pattern(long n, long w, long t, int b);
+// BASELINE config 4: AR1(rho, nt) (x) SPDE(nx x ny lattice) latent field plus p
+// fixed effects, as the joint INLA precision (kronecker.cpp).
+HostMatrix generate_kronecker(int nt, int nx, int ny, int p, double rho, double kappa2, double tau, double tau_y,
+                              double q_beta, uint64_t seed, int b);
 HostMatrix matrix_from_dense(long n, int b, const double* a);  // module.cpp:46-74
 HostMatrix matrix_from_tiles(long n, int b, long count, const int* ti, const int* tj,
                              const double* payload);

@@ -20,6 +20,8 @@ this; it only reads the committed fixtures.
                   tile (Frobenius norm, sum, weighted sum), and the leading /
                   trailing 64 x 64 blocks of sampled tiles (last three tile
                   columns, the middle column, arrow tiles).  Large takes ~4 min.
+                  kron_small / kron_mid: config 4 (AR1 x SPDE + fixed
+                  effects) at reduced scale through read_matrix_market_file
     python tests/golden/make_golden.py configs [DIR]   (DIR: reuse outputs of
     an earlier `ref_driver golden` run written as DIR/<name>.*)
 """
@@ -68,8 +70,16 @@ CONFIGS = {
 }
 
 
+# BASELINE config 4 at reduced scale (the reference reads these as Matrix Market
+# written by this package's generator; it has no Kronecker generator of its own):
+# name: nt, nx, ny, p, b  (rho 0.9, kappa2 0.5, tau 1, tau_y 1, q_beta 0.01, seed 42)
+KRON = {
+    "kron_small": (10, 20, 20, 20, 128),
+    "kron_mid": (50, 40, 25, 20, 256),
+}
+
+
 def pack_config(name, prefix, info, args):
-    n, w, t, b, seed = args
     s = info["block"]
     sampled = np.array(info["sampled"], dtype=np.int32).reshape(-1, 2)
     np.savez_compressed(
@@ -96,6 +106,21 @@ def configs(from_dir=None):
                 out = subprocess.run([os.path.join(REF, "ref_driver"), "golden", str(n), str(w), str(t), str(b),
                                       str(seed), str(os.cpu_count()), prefix],
                                      check=True, capture_output=True, text=True).stdout
+                info = json.loads(out)
+            pack_config(name, prefix, info, args)
+            print("config", name, "logdet", info["logdet"])
+        sys.path.insert(0, ROOT)
+        import paper_2504_19171_b200 as tib
+        for name, args in KRON.items():
+            nt, nx, ny, p, b = args
+            if from_dir:
+                prefix = os.path.join(from_dir, name)
+                info = json.load(open(prefix + ".json"))
+            else:
+                prefix = os.path.join(tmp, name)
+                tib.write_matrix_market(tib.generate_kronecker(nt, nx, ny, p, tile_size=b), prefix + ".mtx")
+                out = subprocess.run([os.path.join(REF, "ref_driver"), "golden_mm", prefix + ".mtx", str(b),
+                                      str(os.cpu_count()), prefix], check=True, capture_output=True, text=True).stdout
                 info = json.loads(out)
             pack_config(name, prefix, info, args)
             print("config", name, "logdet", info["logdet"])
