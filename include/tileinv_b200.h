@@ -116,6 +116,28 @@ int tib_factor_tiles(tib_factor f, int phase, int* ti, int* tj, double* payload)
 /* payload_checksum (storage.cpp:34-48) of the L tiles as stored here.         */
 int tib_factor_checksum(tib_factor f, uint64_t* out);
 int tib_factor_free(tib_factor f);
+/* PhaseTag of the factor's tiles (storage.hpp:11-16): 1 = kFactor (L and the
+ * phase-1 tiles on the device), 2 = kPhase1 (phase-1 tiles only).          */
+int tib_factor_phase(tib_factor f, int* phase);
+/* factor_from_tile_file (tileio.cpp:109-117) from host tiles: phase 1 = the
+ * factor L (phase 1 then runs on the device), phase 2 = phase-1 tiles U / W
+ * (selected inversion skips phase 1 for them, selinv.cpp:355).  Tiles are
+ * b*b row-major in any order; every diagonal tile must be present.         */
+int tib_factor_from_tiles(long n, int tile_size, int phase, long count, const int* ti, const int* tj,
+                          const double* payload, int device, tib_factor* out);
+
+/* ---- STLS tile files (tileio.cpp:30-94, tileio.hpp:9-15), byte-compatible - */
+/* "STLS" | u32 version 1 | n | b | N | phase | count, then per tile (column-
+ * major) u32 i, u32 j, b*b float64.  Read errors: TIB_ERR_PARSE (bad magic,
+ * version, truncation, grid mismatch, upper-triangle tile, unknown phase),
+ * TIB_ERR_FORMAT (a file of the wrong phase for the call).                  */
+int tib_matrix_read_stls(const char* path, tib_matrix* out);      /* matrix_from_tile_file */
+int tib_matrix_write_stls(tib_matrix m, const char* path);         /* write_tile_file, kMatrix */
+/* factor_from_tile_file: kFactor (L) or kPhase1 (U / W) files; the factor
+ * lives on `device` (the --factor reuse of tileinv_main.cpp:183-185).       */
+int tib_factor_read_stls(const char* path, int device, tib_factor* out);
+/* phase 1: the factor L as kFactor; phase 2: the phase-1 tiles as kPhase1. */
+int tib_factor_write_stls(tib_factor f, int phase, const char* path);
 
 /* ---- selected inversion (selinv.hpp:70-85) -------------------------------- */
 /* selected_inverse(const TiledSymmetricMatrix&, request, workers)
@@ -138,6 +160,8 @@ int tib_sigma_entries(tib_sigma s, long* count, long* rows, long* cols, double* 
 int tib_sigma_tiles(tib_sigma s, int* ti, int* tj, double* payload);
 /* payload_checksum (storage.cpp:34-48) of the result tiles.                   */
 int tib_sigma_checksum(tib_sigma s, uint64_t* out);
+/* write_selected_inverse (selinv.cpp:441): the closure tiles, kSelectedInverse. */
+int tib_sigma_write_stls(tib_sigma s, const char* path);
 int tib_sigma_free(tib_sigma s);
 
 /* ---- batched selected inversion (INLA hyper-parameter sweeps) -------------- */

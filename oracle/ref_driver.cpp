@@ -33,6 +33,7 @@
 #include "tileinv/cholesky.hpp"
 #include "tileinv/matgen.hpp"
 #include "tileinv/selinv.hpp"
+#include "tileinv/tileio.hpp"
 
 using namespace tileinv;
 using Clock = std::chrono::steady_clock;
@@ -249,6 +250,23 @@ int main(int argc, char** argv) {
   if (argc >= 6 && std::string(argv[1]) == "golden_mm") {
     const TiledSymmetricMatrix m = read_matrix_market_file(argv[2], std::atoi(argv[3]));
     return golden_run(m, std::atoi(argv[4]), argv[5]);
+  }
+  // ref_driver stls n w t b seed prefix: the reference's own tile files of one
+  // case -- <prefix>.matrix.stls (kMatrix), .factor.stls (kFactor, factorize),
+  // .phase1.stls (kPhase1, phase1), .sigma.stls (write_selected_inverse, pattern)
+  if (argc >= 8 && std::string(argv[1]) == "stls") {
+    GeneratedMatrix gen = generate_arrowhead(
+        {std::atol(argv[2]), std::atol(argv[3]), std::atol(argv[4]), 1.0, std::strtoull(argv[6], nullptr, 10)},
+        std::atoi(argv[5]));
+    const std::string pre = argv[7];
+    write_tile_file(pre + ".matrix.stls", gen.matrix.layout, PhaseTag::kMatrix, gen.matrix.blocks);
+    TiledFactor f = factorize(gen.matrix, symbolic_cholesky(gen.matrix.pattern), 1);
+    write_tile_file(pre + ".factor.stls", f.layout, f.phase, f.blocks);
+    TiledFactor p1 = phase1(f, 1);
+    write_tile_file(pre + ".phase1.stls", p1.layout, p1.phase, p1.blocks);
+    const SelectedInverse s = selected_inverse(f, SelectionRequest::factor_pattern(), 1);
+    write_selected_inverse(pre + ".sigma.stls", s);
+    return 0;
   }
   // ref_driver checksum n w t b seed [density]: payload_checksum of the generated matrix
   if (argc >= 7 && std::string(argv[1]) == "checksum") {

@@ -134,6 +134,10 @@ class Matrix:
         _check(lib.tib_matrix_checksum(self._h, C.byref(out)))
         return out.value
 
+    def write_tiles(self, path: str) -> None:
+        """STLS tile file, kMatrix (write_tile_file, tileio.cpp:30-53)."""
+        _check(lib.tib_matrix_write_stls(self._h, path.encode()))
+
     def to_dense(self) -> np.ndarray:
         """dense_from_tiled (oracle.cpp:24-45), with the reference's n <= 4000 guard."""
         n, b, N, s = self._info()
@@ -183,6 +187,18 @@ class Factor:
         _check(lib.tib_factor_logdet(self._h, C.byref(out)))
         return out.value
 
+    @property
+    def phase(self) -> int:
+        """PhaseTag of the held tiles: 1 kFactor (L + phase-1 tiles), 2 kPhase1."""
+        out = C.c_int()
+        _check(lib.tib_factor_phase(self._h, C.byref(out)))
+        return out.value
+
+    def write_tiles(self, path: str, phase: int = 1) -> None:
+        """STLS tile file (write_tile_file, tileio.cpp:30-53): phase 1 writes L
+        (kFactor), phase 2 the phase-1 tiles U / W (kPhase1)."""
+        _check(lib.tib_factor_write_stls(self._h, phase, path.encode()))
+
     def tiles(self, phase: int = 1):
         """phase 1: L tiles; phase 2: phase-1 tiles (U on the diagonal, W off it)."""
         n, b, s = self._info()
@@ -229,6 +245,11 @@ class SelectedInverseResult:
         out = C.c_uint64()
         _check(lib.tib_sigma_checksum(self._h, C.byref(out)))
         return out.value
+
+    def write_tiles(self, path: str) -> None:
+        """write_selected_inverse (selinv.cpp:441): the closure tiles as an STLS
+        file tagged kSelectedInverse."""
+        _check(lib.tib_sigma_write_stls(self._h, path.encode()))
 
     def entries_arrays(self):
         """extract_entries (selinv.cpp:387-439) as (rows, cols, values) numpy arrays."""
@@ -372,6 +393,33 @@ def write_matrix_market(matrix: Matrix, path: str) -> None:
             f.write(buf.raw[: size.value])
     except OSError:
         raise TileinvError(f"cannot open {path} for writing") from None
+
+
+def read_matrix_tiles(path: str) -> Matrix:
+    """matrix_from_tile_file(read_tile_file(path)) (tileio.cpp:55-107)."""
+    h = _new_handle()
+    _check(lib.tib_matrix_read_stls(path.encode(), C.byref(h)))
+    return Matrix(h.value)
+
+
+def read_factor_tiles(path: str, device: int = 0) -> Factor:
+    """factor_from_tile_file(read_tile_file(path)): a kFactor or kPhase1 file,
+    resident on `device` (the CLI's ``selinv --factor``)."""
+    h = _new_handle()
+    _check(lib.tib_factor_read_stls(path.encode(), device, C.byref(h)))
+    return Factor(h.value)
+
+
+def factor_from_tiles(n: int, tile_size: int, ti, tj, payload, phase: int = 1, device: int = 0) -> Factor:
+    """A factor from host tiles: phase 1 = L (kFactor), 2 = U / W (kPhase1)."""
+    ti = np.ascontiguousarray(ti, dtype=np.int32)
+    tj = np.ascontiguousarray(tj, dtype=np.int32)
+    pay = np.ascontiguousarray(payload, dtype=np.float64)
+    h = _new_handle()
+    _check(lib.tib_factor_from_tiles(n, tile_size, phase, len(ti), ti.ctypes.data_as(C.POINTER(C.c_int)),
+                                     tj.ctypes.data_as(C.POINTER(C.c_int)),
+                                     pay.ctypes.data_as(C.POINTER(C.c_double)), device, C.byref(h)))
+    return Factor(h.value)
 
 
 def factorize(matrix: Matrix, workers: int = 1, device: int = 0) -> Factor:

@@ -56,6 +56,13 @@ SIGNATURES = {
     "tib_factor_tiles": [_p, _i, _pi, _pi, _pd],
     "tib_factor_checksum": [_p, _pu64],
     "tib_factor_free": [_p],
+    "tib_factor_phase": [_p, _pi],
+    "tib_factor_from_tiles": [_l, _i, _i, _l, _pi, _pi, _pd, _i, _pp],
+    "tib_factor_read_stls": [C.c_char_p, _i, _pp],
+    "tib_factor_write_stls": [_p, _i, C.c_char_p],
+    "tib_matrix_read_stls": [C.c_char_p, _pp],
+    "tib_matrix_write_stls": [_p, C.c_char_p],
+    "tib_sigma_write_stls": [_p, C.c_char_p],
     "tib_selected_inverse": [_p, _i, _pl, _pl, _l, _i, _pp],
     "tib_selected_inverse_of_factor": [_p, _i, _pl, _pl, _l, _pp],
     "tib_sigma_info": [_p, _pl, _pi, _pl, _pi],

@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <functional>
 #include <atomic>
 #include <climits>
@@ -155,11 +156,12 @@ struct HostBuf {
 
 // ---------------------------------------------------------------------------
 // per-device runtime
+constexpr int kOnes = 256;
 struct DeviceRt {
   int dev = -1;
   cudaStream_t stream = nullptr;
   cudaStream_t upload = nullptr;  // streamed H2D of the A store, concurrent with the factor sweep
-  int* one = nullptr;             // pinned host 1: the copy engine writes it into upload counters
+  int* one = nullptr;             // pinned host 1s (kOnes): the copy engine writes them into upload counters
   bool ready = false;
 };
 static std::mutex g_rt_mu;
@@ -183,8 +185,8 @@ static DeviceRt& runtime(int device) {
     CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
     CK(cudaStreamCreateWithFlags(&rt.stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&rt.upload, cudaStreamNonBlocking));
-    CK(cudaMallocHost(reinterpret_cast<void**>(&rt.one), sizeof(int)));
-    *rt.one = 1;
+    CK(cudaMallocHost(reinterpret_cast<void**>(&rt.one), kOnes * sizeof(int)));
+    for (int i = 0; i < kOnes; ++i) rt.one[i] = 1;
     CK(static_cast<cudaError_t>(configure_kernels()));
     rt.dev = device;
     rt.ready = true;
@@ -334,6 +336,21 @@ static std::shared_ptr<Phase2Plan> phase2_plan_for(const Pattern& F, const Closu
   std::lock_guard<std::mutex> lk(g_plan_mu);
   if (g_p2plans.size() > 16) g_p2plans.clear();
   g_p2plans[{device, key}] = plan;
+  return plan;
+}
+
+static std::map<std::pair<int, uint64_t>, std::shared_ptr<DevPlan>> g_p1plans;
+static std::shared_ptr<DevPlan> phase1_plan_for(const Pattern& F, int device, cudaStream_t s) {
+  const uint64_t key = pattern_hash(F, 3);
+  {
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    auto it = g_p1plans.find({device, key});
+    if (it != g_p1plans.end()) return it->second;
+  }
+  auto plan = upload_plan(build_phase1_dataflow(F), device, s);
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  if (g_p1plans.size() > 8) g_p1plans.clear();
+  g_p1plans[{device, key}] = plan;
   return plan;
 }
 
@@ -510,6 +527,26 @@ static void run_flow_chunked(DevPlan& P, const std::vector<BaseTable>& tables, c
   }
 }
 
+// TIB_HOST_TIMING=1: wall-clock phase marks of a public call on stderr (each
+// mark synchronises the stream, so only for diagnosis).
+struct HostTimer {
+  bool on;
+  cudaStream_t s;
+  std::chrono::steady_clock::time_point t0, last;
+  explicit HostTimer(cudaStream_t st) : on(env_int("TIB_HOST_TIMING", 0) != 0), s(st) {
+    t0 = last = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[tib timing] %-28s %9.3f ms (total %9.3f)\n", what,
+                 std::chrono::duration<double, std::milli>(now - last).count(),
+                 std::chrono::duration<double, std::milli>(now - t0).count());
+    last = now;
+  }
+};
+
 // ---------------------------------------------------------------------------
 // objects behind the handles
 struct MatrixObj {
@@ -530,22 +567,19 @@ struct MatrixObj {
 // Generator on the device (generate.cu) into a tile store over `pat` with row
 // stride bp (identity padding), stream-ordered.
 static void device_generate(const MatrixObj& m, const Pattern& pat, int bp, double* out, cudaStream_t s) {
-  std::vector<int> ti(pat.size()), tj(pat.size());
-  for (size_t k = 0; k < pat.size(); ++k) {
-    ti[k] = pat.tiles()[k].i;
-    tj[k] = pat.tiles()[k].j;
-  }
-  int* d_ij = nullptr;
-  double* d_diag = nullptr;
-  CK(cudaMallocAsync(reinterpret_cast<void**>(&d_ij), 2 * pat.size() * sizeof(int), s));
-  CK(cudaMallocAsync(reinterpret_cast<void**>(&d_diag), static_cast<size_t>(m.gen.n) * sizeof(double), s));
-  CK(cudaMemcpyAsync(d_ij, ti.data(), ti.size() * sizeof(int), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(d_ij + pat.size(), tj.data(), tj.size() * sizeof(int), cudaMemcpyHostToDevice, s));
-  CK(static_cast<cudaError_t>(launch_generate_arrowhead(m.gen.n, m.gen.w, m.gen.t, m.gen.seed, m.layout.b, bp, d_ij,
-                                                        d_ij + pat.size(), static_cast<long>(pat.size()), d_diag, out, s)));
-  CK(cudaFreeAsync(d_ij, s));
-  CK(cudaFreeAsync(d_diag, s));
-  CK(cudaStreamSynchronize(s));  // the host vectors above die with this scope
+  const int N = pat.layout().N;
+  std::vector<int> meta(static_cast<size_t>(N) + 1 + pat.size());  // colptr (N + 1), then rows
+  int maxc = 0;
+  for (int j = 0; j <= N; ++j) meta[static_cast<size_t>(j)] = static_cast<int>(pat.col_start(j));
+  for (int j = 0; j < N; ++j) maxc = std::max(maxc, static_cast<int>(pat.col_start(j + 1) - pat.col_start(j)));
+  for (size_t k = 0; k < pat.size(); ++k) meta[static_cast<size_t>(N) + 1 + k] = pat.tiles()[k].i;
+  int* d_meta = nullptr;
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&d_meta), meta.size() * sizeof(int), s));
+  CK(cudaMemcpyAsync(d_meta, meta.data(), meta.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+  CK(static_cast<cudaError_t>(launch_generate_arrowhead(m.gen.n, m.gen.w, m.gen.t, m.gen.seed, m.layout.b, bp, N,
+                                                        d_meta, d_meta + N + 1, maxc, out, s)));
+  CK(cudaFreeAsync(d_meta, s));
+  CK(cudaStreamSynchronize(s));  // the host vector above dies with this scope
 }
 
 static DeviceRt& runtime(int device);
@@ -564,10 +598,15 @@ static const double* host_payload(const MatrixObj& m) {
   return m.payload.p;
 }
 
+// TiledFactor (storage.hpp:46-51), device resident.  has_L: the factor tiles L
+// are held (PhaseTag kFactor -- factorize, or a kFactor tile file); without,
+// only the phase-1 tiles (a kPhase1 tile file: U_j = X_j^T and W_kj).
 struct FactorObj {
   int device = 0;
   Layout layout;
-  std::shared_ptr<FactorPlan2> plan;
+  Pattern F;  // the factor's (filled) tile pattern
+  int bp = 0, nb = 0;
+  bool has_L = true;
   DevBuf L, P1;
   double logdet = 0;
 };
@@ -591,6 +630,37 @@ static void fill_matrix(MatrixObj& m, HostMatrix&& hm) {
 
 // Host matrix -> bp-layout A store over the FILLED pattern (fill-in tiles zero,
 // identity on the padded diagonal).
+// Uploads the filled-pattern slots of tile columns [c0, c1) of m (b = bp): runs
+// of slots present in m's pattern with consecutive host slots are one H2D
+// copy (copies = true), runs of fill-in slots one memset (zeros = true) -- no
+// host staging.  A streamed upload issues the memsets on the sweep stream
+// before the sweep: a memset is a kernel and cannot start while the persistent
+// sweep holds every SM, so on the copy stream it would stall the copies behind it.
+static void upload_columns(const MatrixObj& m, const Pattern& F, int c0, int c1, double* dA, cudaStream_t s,
+                           bool copies = true, bool zeros = true) {
+  const size_t bb = static_cast<size_t>(m.layout.b) * m.layout.b;
+  long k = F.col_start(c0);
+  const long kend = F.col_start(c1);
+  while (k < kend) {
+    const long src = m.pattern.slot(F.tiles()[static_cast<size_t>(k)].i, F.tiles()[static_cast<size_t>(k)].j);
+    long e = k + 1;
+    if (src >= 0) {
+      while (e < kend && m.pattern.slot(F.tiles()[static_cast<size_t>(e)].i, F.tiles()[static_cast<size_t>(e)].j) ==
+                             src + (e - k))
+        ++e;
+      if (copies)
+        CK(cudaMemcpyAsync(dA + static_cast<size_t>(k) * bb, m.payload.p + static_cast<size_t>(src) * bb,
+                           static_cast<size_t>(e - k) * bb * sizeof(double), cudaMemcpyHostToDevice, s));
+    } else {
+      while (e < kend && m.pattern.slot(F.tiles()[static_cast<size_t>(e)].i, F.tiles()[static_cast<size_t>(e)].j) < 0)
+        ++e;
+      if (zeros)
+        CK(cudaMemsetAsync(dA + static_cast<size_t>(k) * bb, 0, static_cast<size_t>(e - k) * bb * sizeof(double), s));
+    }
+    k = e;
+  }
+}
+
 static void upload_matrix(const MatrixObj& m, const Pattern& filled, int bp, double* dA, cudaStream_t s,
                           HostBuf* staging_keep = nullptr) {
   if (m.gen.on) {  // no host values: generate in place
@@ -601,6 +671,11 @@ static void upload_matrix(const MatrixObj& m, const Pattern& filled, int bp, dou
   const size_t bb = static_cast<size_t>(b) * b, bpp = static_cast<size_t>(bp) * bp;
   if (bp == b && filled == m.pattern) {
     CK(cudaMemcpyAsync(dA, m.payload.p, filled.size() * bb * sizeof(double), cudaMemcpyHostToDevice, s));
+    return;
+  }
+  if (bp == b && m.payload.pinned) {
+    upload_columns(m, filled, 0, m.layout.N, dA, s);
+    CK(cudaStreamSynchronize(s));
     return;
   }
   HostBuf local;
@@ -724,16 +799,20 @@ static Request make_request(int preset, const long* rows, const long* cols, long
 static SigmaObj* selected_inverse_matrix(const MatrixObj& m, const Request& req, int device) {
   DeviceRt& rt = runtime(device);
   cudaStream_t s = rt.stream;
+  HostTimer tm(s);
   auto fp = factor_plan_for(m.pattern, device, s);
   const Pattern& F = fp->sym.filled;
   const Closure sel = symbolic_inversion(select_tiles(F.layout(), F, req), F);
   auto p2 = phase2_plan_for(F, sel, device, s);
+  tm.mark("plans");
   SweepStores st;
   alloc_factor_stores(st, *fp, 1, device, s, p2->flow->host.counters, p2->flow->host.scratch_doubles);
+  tm.mark("allocations");
   // The A store goes up tile column by tile column on the upload stream while
   // the factor sweep runs (tasks poll each column's counter); only possible
-  // when the host payload already has the device layout (b = bp, no fill-in).
-  const bool stream_up = !m.gen.on && fp->bp == m.layout.b && F == m.pattern && m.payload.pinned &&
+  // when the host tiles already have the device layout (b = bp; fill-in slots
+  // are zeroed on the upload stream).
+  const bool stream_up = !m.gen.on && fp->bp == m.layout.b && m.payload.pinned &&
                          env_int("TIB_STREAM_UPLOAD", 1) != 0 && fp->flow->host.upl >= 0;
   if (!stream_up) upload_matrix(m, F, fp->bp, st.A.p, s);
   auto* res = new SigmaObj;
@@ -753,12 +832,17 @@ static SigmaObj* selected_inverse_matrix(const MatrixObj& m, const Request& req,
     const size_t bb = static_cast<size_t>(fp->bp) * fp->bp;
     int* upl = reinterpret_cast<int*>(st.ctr(0)) + fp->flow->host.upl;
     std::function<void()> up = [&]() {
+      const bool same = F == m.pattern;
+      if (!same) upload_columns(m, F, 0, m.layout.N, st.A.p, s, false, true);
       CK(cudaEventRecord(cleared, s));
       CK(cudaStreamWaitEvent(rt.upload, cleared, 0));
       for (int c = 0; c < m.layout.N; ++c) {
         const size_t t0 = static_cast<size_t>(F.col_start(c)), t1 = static_cast<size_t>(F.col_start(c + 1));
-        CK(cudaMemcpyAsync(st.A.p + t0 * bb, m.payload.p + t0 * bb, (t1 - t0) * bb * sizeof(double),
-                           cudaMemcpyHostToDevice, rt.upload));
+        if (same)
+          CK(cudaMemcpyAsync(st.A.p + t0 * bb, m.payload.p + t0 * bb, (t1 - t0) * bb * sizeof(double),
+                             cudaMemcpyHostToDevice, rt.upload));
+        else
+          upload_columns(m, F, c, c + 1, st.A.p, rt.upload, true, false);
         CK(cudaMemcpyAsync(upl + c, rt.one, sizeof(int), cudaMemcpyHostToDevice, rt.upload));
       }
       CK(cudaEventRecord(uploaded, rt.upload));
@@ -768,12 +852,16 @@ static SigmaObj* selected_inverse_matrix(const MatrixObj& m, const Request& req,
     cudaEventDestroy(cleared);
     cudaEventDestroy(uploaded);
   } else {
+    tm.mark("upload");
     factor_sweep(*fp, st, s, tables);
   }
+  tm.mark("factor sweep");
   phase2_sweep(*p2, s, tables);
+  tm.mark("phase-2 sweep");
   std::vector<double> parts(fp->flow->host.logdet_doubles);
   CK(cudaMemcpyAsync(parts.data(), st.logdet.p, parts.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
   check_status(st.status, 1, m.layout, s);
+  tm.mark("read-back");
   res->logdet = reduce_logdet(parts.data(), m.layout.N, fp->nb);
   return guard.release();
 }
@@ -822,6 +910,78 @@ static uint64_t checksum_store(const double* hostbp, const Pattern& pat, int b, 
     for (int r = 0; r < b; ++r) h.mix(src + static_cast<size_t>(r) * bp, b * sizeof(double));
   }
   return h.h;
+}
+
+// Host tiles (reference layout: b*b row-major per slot of F) -> a bp-layout
+// device store; diagonal tiles optionally transposed (U_j -> X_j) and their
+// padding set to the identity (so X = L^{-1} holds on the padded block).
+static void upload_host_tiles(const Pattern& F, int b, int bp, const double* pay, double* dst, cudaStream_t s,
+                              bool transpose_diag) {
+  const size_t bb = static_cast<size_t>(b) * b, bpp = static_cast<size_t>(bp) * bp;
+  HostBuf st(F.size() * bpp);
+  std::memset(st.p, 0, st.n * sizeof(double));
+  for (size_t k = 0; k < F.size(); ++k) {
+    const Coord& c = F.tiles()[k];
+    double* d = st.p + k * bpp;
+    const double* src = pay + k * bb;
+    if (transpose_diag && c.i == c.j) {
+      for (int r = 0; r < b; ++r)
+        for (int q = 0; q < b; ++q) d[static_cast<size_t>(r) * bp + q] = src[static_cast<size_t>(q) * b + r];
+    } else {
+      for (int r = 0; r < b; ++r) std::memcpy(d + static_cast<size_t>(r) * bp, src + static_cast<size_t>(r) * b, b * sizeof(double));
+    }
+    if (c.i == c.j)
+      for (int r = b; r < bp; ++r) d[static_cast<size_t>(r) * bp + r] = 1.0;
+  }
+  CK(cudaMemcpyAsync(dst, st.p, st.n * sizeof(double), cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
+}
+
+// A factor from host tiles (factor_from_tile_file, tileio.cpp:109-117): phase 1
+// = the factor L (phase 1 then runs on the device: build_phase1_dataflow),
+// phase 2 = phase-1 tiles U / W (used as they are; selinv.cpp:355 skips
+// phase 1 for them).  logdet from the diagonal: 2 sum log L_rr = -2 sum log U_rr.
+static FactorObj* factor_from_host(const Layout& L, int phase, const Pattern& P, const double* pay, int device) {
+  if (phase != 1 && phase != 2)
+    throw Error(kErrFormat, "expected a factor tile file, found phase tag " + std::to_string(phase));
+  if (!P.has_all_diagonals()) throw Error(kErrStructure, "factor tiles must include every diagonal tile");
+  DeviceRt& rt = runtime(device);
+  cudaStream_t s = rt.stream;
+  auto f = std::make_unique<FactorObj>();
+  f->device = device;
+  f->layout = L;
+  f->F = P;
+  f->bp = (L.b + 63) / 64 * 64;
+  f->nb = f->bp / 64;
+  const size_t tile = static_cast<size_t>(f->bp) * f->bp, bb = static_cast<size_t>(L.b) * L.b;
+  double ld = 0.0;
+  for (long r = 0; r < L.n; ++r) {
+    const int j = static_cast<int>(r / L.b);
+    const double v = pay[static_cast<size_t>(P.col_start(j)) * bb + static_cast<size_t>(r % L.b) * L.b + (r % L.b)];
+    if (!(v > 0.0)) throw Error(kErrConsistency, "factor diagonal entry " + std::to_string(r) + " is not positive");
+    ld += std::log(v);
+  }
+  f->logdet = phase == 1 ? 2.0 * ld : -2.0 * ld;
+  f->P1 = DevBuf(P.size() * tile, device, s);
+  if (phase == 2) {
+    f->has_L = false;
+    upload_host_tiles(P, L.b, f->bp, pay, f->P1.p, s, true);
+    return f.release();
+  }
+  f->L = DevBuf(P.size() * tile, device, s);
+  upload_host_tiles(P, L.b, f->bp, pay, f->L.p, s, false);
+  auto plan = phase1_plan_for(P, device, s);
+  DevBuf scratch(plan->host.scratch_doubles, device, s);
+  DevBuf logdet(plan->host.logdet_doubles, device, s);
+  DevBuf status(1, device, s);
+  CK(cudaMemsetAsync(status.p, 0xff, sizeof(unsigned long long), s));
+  DevBuf ctr = alloc_counters(plan->host.counters, 1, device, s);
+  // the invert-only leaves read their block through the A-store entry: L
+  std::vector<BaseTable> tables{make_table(f->L.p, f->L.p, f->P1.p, nullptr, nullptr, scratch.p, logdet.p, status.p, ctr.p)};
+  run_flow_chunked(*plan, tables, s);
+  CK(cudaStreamSynchronize(s));
+  check_watchdog();
+  return f.release();
 }
 
 // ---------------------------------------------------------------------------
@@ -1033,7 +1193,9 @@ int tib_factorize(tib_matrix m, int device, tib_factor* out) {
     auto* f = new tib_factor_s;
     f->device = device;
     f->layout = m->layout;
-    f->plan = fp;
+    f->F = fp->sym.filled;
+    f->bp = fp->bp;
+    f->nb = fp->nb;
     f->L = std::move(st.L);
     f->P1 = std::move(st.P1);
     f->logdet = reduce_logdet(parts.data(), m->layout.N, fp->nb);
@@ -1045,7 +1207,7 @@ int tib_factor_info(tib_factor f, long* n, int* b, long* stored) {
     need(f, "factor");
     if (n) *n = f->layout.n;
     if (b) *b = f->layout.b;
-    if (stored) *stored = static_cast<long>(f->plan->sym.filled.size());
+    if (stored) *stored = static_cast<long>(f->F.size());
   });
 }
 int tib_factor_logdet(tib_factor f, double* out) {
@@ -1055,24 +1217,97 @@ int tib_factor_tiles(tib_factor f, int phase, int* ti, int* tj, double* payload)
   return guarded([&] {
     need(f, "factor");
     if (phase != 1 && phase != 2) throw Error(kErrInvalidArgument, "phase must be 1 (factor) or 2 (phase-1 tiles)");
+    if (phase == 1 && !f->has_L) throw Error(kErrContract, "the factor holds phase-1 tiles only (kPhase1 input)");
     DeviceRt& rt = runtime(f->device);
-    download_tiles(phase == 1 ? f->L : f->P1, f->plan->sym.filled, f->layout.b, f->plan->bp, ti, tj, payload, rt.stream,
-                   phase == 2);
+    download_tiles(phase == 1 ? f->L : f->P1, f->F, f->layout.b, f->bp, ti, tj, payload, rt.stream, phase == 2);
   });
 }
 int tib_factor_checksum(tib_factor f, uint64_t* out) {
   return guarded([&] {
     need(f, "factor");
     DeviceRt& rt = runtime(f->device);
-    HostBuf h(f->L.n);
-    CK(cudaMemcpyAsync(h.p, f->L.p, h.n * sizeof(double), cudaMemcpyDeviceToHost, rt.stream));
-    CK(cudaStreamSynchronize(rt.stream));
-    *out = checksum_store(h.p, f->plan->sym.filled, f->layout.b, f->plan->bp);
+    if (f->has_L) {
+      HostBuf h(f->L.n);
+      CK(cudaMemcpyAsync(h.p, f->L.p, h.n * sizeof(double), cudaMemcpyDeviceToHost, rt.stream));
+      CK(cudaStreamSynchronize(rt.stream));
+      *out = checksum_store(h.p, f->F, f->layout.b, f->bp);
+    } else {  // the phase-1 tiles in the reference's form (U_j = X_j^T)
+      const size_t bb = static_cast<size_t>(f->layout.b) * f->layout.b;
+      std::vector<double> pay(f->F.size() * bb);
+      download_tiles(f->P1, f->F, f->layout.b, f->bp, nullptr, nullptr, pay.data(), rt.stream, true);
+      *out = checksum_store(pay.data(), f->F, f->layout.b, f->layout.b);
+    }
   });
 }
 int tib_factor_free(tib_factor f) {
   delete f;
   return kOk;
+}
+int tib_factor_phase(tib_factor f, int* phase) {
+  return guarded([&] { *phase = need(f, "factor")->has_L ? 1 : 2; });
+}
+int tib_factor_from_tiles(long n, int b, int phase, long count, const int* ti, const int* tj, const double* payload,
+                          int device, tib_factor* out) {
+  return guarded([&] {
+    if (count < 1 || !ti || !tj || !payload) throw Error(kErrInvalidArgument, "factor tiles are empty");
+    const Layout L = build_layout(n, b);
+    std::vector<Coord> c(static_cast<size_t>(count));
+    for (long k = 0; k < count; ++k) c[static_cast<size_t>(k)] = {ti[k], tj[k]};
+    const Pattern P(L, c);
+    if (static_cast<long>(P.size()) != count) throw Error(kErrInvalidArgument, "duplicate factor tiles");
+    const size_t bb = static_cast<size_t>(b) * b;
+    std::vector<double> pay(P.size() * bb);
+    for (long k = 0; k < count; ++k)
+      std::memcpy(&pay[static_cast<size_t>(P.slot(ti[k], tj[k])) * bb], payload + static_cast<size_t>(k) * bb, bb * sizeof(double));
+    FactorObj* f = factor_from_host(L, phase, P, pay.data(), device);
+    auto* o = new tib_factor_s;
+    static_cast<FactorObj&>(*o) = std::move(*f);
+    delete f;
+    *out = o;
+  });
+}
+int tib_factor_read_stls(const char* path, int device, tib_factor* out) {
+  return guarded([&] {
+    if (!path) throw Error(kErrInvalidArgument, "null path");
+    const TileFileData d = read_tile_file(path);
+    FactorObj* f = factor_from_host(d.layout, d.phase, d.pattern, d.payload.data(), device);
+    auto* o = new tib_factor_s;
+    static_cast<FactorObj&>(*o) = std::move(*f);
+    delete f;
+    *out = o;
+  });
+}
+int tib_factor_write_stls(tib_factor f, int phase, const char* path) {
+  return guarded([&] {
+    need(f, "factor");
+    if (!path) throw Error(kErrInvalidArgument, "null path");
+    if (phase != 1 && phase != 2) throw Error(kErrInvalidArgument, "phase must be 1 (factor) or 2 (phase-1 tiles)");
+    if (phase == 1 && !f->has_L) throw Error(kErrContract, "the factor holds phase-1 tiles only (kPhase1 input)");
+    DeviceRt& rt = runtime(f->device);
+    const size_t bb = static_cast<size_t>(f->layout.b) * f->layout.b;
+    std::vector<double> pay(f->F.size() * bb);
+    download_tiles(phase == 1 ? f->L : f->P1, f->F, f->layout.b, f->bp, nullptr, nullptr, pay.data(), rt.stream, phase == 2);
+    write_tile_file(path, f->layout, phase, f->F, pay.data());
+  });
+}
+int tib_matrix_read_stls(const char* path, tib_matrix* out) {
+  return guarded([&] {
+    if (!path) throw Error(kErrInvalidArgument, "null path");
+    TileFileData d = read_tile_file(path);
+    if (d.phase != 0) throw Error(kErrFormat, "expected a matrix tile file, found phase tag " + std::to_string(d.phase));
+    HostMatrix hm;
+    hm.layout = d.layout;
+    hm.pattern = std::move(d.pattern);
+    hm.payload = std::move(d.payload);
+    *out = wrap(std::move(hm));
+  });
+}
+int tib_matrix_write_stls(tib_matrix m, const char* path) {
+  return guarded([&] {
+    need(m, "matrix");
+    if (!path) throw Error(kErrInvalidArgument, "null path");
+    write_tile_file(path, m->layout, 0, m->pattern, host_payload(*m));
+  });
 }
 
 int tib_selected_inverse(tib_matrix m, int preset, const long* rows, const long* cols, long ne, int device,
@@ -1095,7 +1330,7 @@ int tib_selected_inverse_of_factor(tib_factor f, int preset, const long* rows, c
     DeviceRt& rt = runtime(f->device);
     cudaStream_t s = rt.stream;
     const Request req = make_request(preset, rows, cols, ne);
-    const Pattern& F = f->plan->sym.filled;
+    const Pattern& F = f->F;
     const Closure sel = symbolic_inversion(select_tiles(F.layout(), F, req), F);
     auto p2 = phase2_plan_for(F, sel, f->device, s);
     auto* res = new tib_sigma_s;
@@ -1185,6 +1420,18 @@ int tib_sigma_checksum(tib_sigma sg, uint64_t* out) {
     *out = checksum_store(sigma_host(*sg), sg->plan->sel.closure, sg->layout.b, sg->plan->bp);
   });
 }
+int tib_sigma_write_stls(tib_sigma sg, const char* path) {
+  return guarded([&] {
+    need(sg, "result");
+    if (!path) throw Error(kErrInvalidArgument, "null path");
+    DeviceRt& rt = runtime(sg->device);
+    const Pattern& C = sg->plan->sel.closure;
+    const size_t bb = static_cast<size_t>(sg->layout.b) * sg->layout.b;
+    std::vector<double> pay(C.size() * bb);
+    download_tiles(sg->S, C, sg->layout.b, sg->plan->bp, nullptr, nullptr, pay.data(), rt.stream, false);
+    write_tile_file(path, sg->layout, 3, C, pay.data());
+  });
+}
 int tib_sigma_free(tib_sigma sg) {
   delete sg;
   return kOk;
@@ -1199,33 +1446,81 @@ int tib_selected_inverse_batch(const tib_matrix* ms, int count, int device, doub
         throw Error(kErrInvalidArgument, "batched matrices must share one tile pattern");
     DeviceRt& rt = runtime(device);
     cudaStream_t s = rt.stream;
+    HostTimer tm(s);
     auto fp = factor_plan_for(m0.pattern, device, s);
     const Pattern& F = fp->sym.filled;
     Request req;
     req.preset = kFactorPattern;
     const Closure sel = symbolic_inversion(select_tiles(F.layout(), F, req), F);
     auto p2 = phase2_plan_for(F, sel, device, s);
+    tm.mark("plans");
     const size_t tile = static_cast<size_t>(fp->bp) * fp->bp;
     SweepStores st;
     alloc_factor_stores(st, *fp, count, device, s, p2->flow->host.counters, p2->flow->host.scratch_doubles);
     DevBuf Sg(p2->sel.closure.size() * tile * count, device, s);
     DevBuf var(static_cast<size_t>(m0.layout.N) * fp->bp * count, device, s);
+    tm.mark("allocations");
     std::vector<BaseTable> tables;
     const size_t T = F.size();
+    // streamed upload (as the single path): tile column c of every matrix goes
+    // up on the copy stream, column-major over the batch, while the batched
+    // factor sweep runs; each matrix's tasks poll that matrix's column counters
+    bool stream_up = fp->bp == m0.layout.b && env_int("TIB_STREAM_UPLOAD", 1) != 0 && fp->flow->host.upl >= 0 &&
+                     static_cast<size_t>(count) <= max_batch(*fp->flow);
+    for (int k = 0; k < count; ++k) stream_up = stream_up && !ms[k]->gen.on && ms[k]->payload.pinned;
     for (int k = 0; k < count; ++k) {
-      upload_matrix(*ms[k], F, fp->bp, st.A.p + T * tile * k, s);
+      if (!stream_up) upload_matrix(*ms[k], F, fp->bp, st.A.p + T * tile * k, s);
       tables.push_back(make_table(st.A.p + T * tile * k, st.L.p + T * tile * k, st.P1.p + T * tile * k,
                                   Sg.p + p2->sel.closure.size() * tile * k, var.p + static_cast<size_t>(m0.layout.N) * fp->bp * k,
                                   st.scratch.p + st.scratch_stride * k,
                                   st.logdet.p + fp->flow->host.logdet_doubles * k, st.status.p + k, st.ctr(k)));
     }
-    factor_sweep(*fp, st, s, tables);
+    if (stream_up) {
+      cudaEvent_t cleared, uploaded;
+      CK(cudaEventCreateWithFlags(&cleared, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&uploaded, cudaEventDisableTiming));
+      const bool same = F == m0.pattern;
+      // groups of columns per copy (~48 groups per matrix): fewer API calls than
+      // the copy engine needs time for, while each chain waits for little more
+      // than its first group
+      const int N = m0.layout.N, grp = std::max(1, std::min(kOnes, (N + 47) / 48));
+      std::function<void()> up = [&]() {
+        if (!same)
+          for (int k = 0; k < count; ++k) upload_columns(*ms[k], F, 0, N, st.A.p + T * tile * k, s, false, true);
+        CK(cudaEventRecord(cleared, s));
+        CK(cudaStreamWaitEvent(rt.upload, cleared, 0));
+        for (int c = 0; c < N; c += grp)
+          for (int k = 0; k < count; ++k) {
+            const int ce = std::min(N, c + grp);
+            double* dA = st.A.p + T * tile * k;
+            const size_t t0 = static_cast<size_t>(F.col_start(c)), t1 = static_cast<size_t>(F.col_start(ce));
+            if (same)
+              CK(cudaMemcpyAsync(dA + t0 * tile, ms[k]->payload.p + t0 * tile, (t1 - t0) * tile * sizeof(double),
+                                 cudaMemcpyHostToDevice, rt.upload));
+            else
+              upload_columns(*ms[k], F, c, ce, dA, rt.upload, true, false);
+            CK(cudaMemcpyAsync(reinterpret_cast<int*>(st.ctr(k)) + fp->flow->host.upl + c, rt.one,
+                               static_cast<size_t>(ce - c) * sizeof(int), cudaMemcpyHostToDevice, rt.upload));
+          }
+        CK(cudaEventRecord(uploaded, rt.upload));
+      };
+      factor_sweep(*fp, st, s, tables, &up);
+      CK(cudaStreamWaitEvent(s, uploaded, 0));
+      cudaEventDestroy(cleared);
+      cudaEventDestroy(uploaded);
+    } else {
+      tm.mark("uploads");
+      factor_sweep(*fp, st, s, tables);
+    }
+    tm.mark("factor sweep");
     phase2_sweep(*p2, s, tables);
+    tm.mark("phase-2 sweep");
     std::vector<double> parts(static_cast<size_t>(m0.layout.N) * fp->nb * count);
     std::vector<double> v(var.n);
     CK(cudaMemcpyAsync(parts.data(), st.logdet.p, parts.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(v.data(), var.p, v.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
     check_status(st.status, count, m0.layout, s);
+    tm.mark("read-back");
     const Layout& L = m0.layout;
     for (int k = 0; k < count; ++k) {
       if (logdet) logdet[k] = reduce_logdet(parts.data() + static_cast<size_t>(L.N) * fp->nb * k, L.N, fp->nb);

@@ -51,8 +51,8 @@ void launch_dataflow(const FlowArgs& a, const int* need, const int* init0, int n
 void launch_zero_strips(const ZeroStrip* z, int count, int ld, int batch, const BaseTable* tables, cudaStream_t s);
 void launch_fill(double* p, double v, size_t count, cudaStream_t s);
 // generate.cu: density-1 arrowhead generator (matgen.cpp:59-120) into a tile
-// store over the given slots (row stride bp); diag_scratch holds n doubles.
-int launch_generate_arrowhead(long n, long w, long t, unsigned long long seed, int b, int bp, const int* slot_ti,
-                              const int* slot_tj, long slots, double* diag_scratch, double* out, cudaStream_t s);
+// store over a pattern given as device CSC (colptr[N + 1], rows), row stride bp.
+int launch_generate_arrowhead(long n, long w, long t, unsigned long long seed, int b, int bp, int N, const int* colptr,
+                              const int* rows, int max_col_slots, double* out, cudaStream_t s);
 
 }  // namespace tib

@@ -751,6 +751,88 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
   return P;
 }
 
+DataflowPlan build_phase1_dataflow(const Pattern& F) {
+  DataflowPlan P;
+  P.L = F.layout();
+  const Layout& L = P.L;
+  const int bp = (L.b + kB - 1) / kB * kB, nb = bp / kB, NB2 = nb * nb;
+  P.bp = bp;
+  P.nb = nb;
+  const long T = static_cast<long>(F.size());
+  const int N = L.N;
+  // counters: X blocks and per-column X completion, T-term accumulation
+  // ordinals, W completion per tile
+  const long cXblk = 0, cXfin = cXblk + static_cast<long>(N) * NB2, cTblk = cXfin + N,
+             cWfin = cTblk + static_cast<long>(N) * NB2, cEnd = cWfin + T;
+  P.counters = cEnd;
+  const size_t t_doubles = static_cast<size_t>(N) * bp * bp;
+  P.scratch_doubles = t_doubles;
+  P.logdet_doubles = static_cast<size_t>(N) * nb;
+  auto xblk = [&](int j, int p, int q) { return static_cast<int>(cXblk + static_cast<long>(j) * NB2 + p * nb + q); };
+  auto xfin = [&](int j) { return static_cast<int>(cXfin + j); };
+  auto tcnt = [&](int j, int p, int q) { return static_cast<int>(cTblk + static_cast<long>(j) * NB2 + p * nb + q); };
+  auto wfin = [&](long s) { return static_cast<int>(cWfin + s); };
+  const int xdone = nb * (nb + 1) / 2;
+  const long long tsz = static_cast<long long>(bp) * bp;
+  P.slot_tiles = F.tiles();
+  Builder B(P);
+  for (int j = 0; j < N; ++j) {
+    const long ds = F.col_start(j);
+    const int valid = static_cast<int>(std::min<long>(L.b, L.n - static_cast<long>(j) * L.b));
+    // X_j = L_jj^{-1}: every 64-block leaf inverts its (given) diagonal block of L
+    // at once; the blocks below the diagonal follow right-looking, T(kk, k) =
+    // sum_{l=k}^{kk-1} L(kk, l) X(l, k) term by term, X(kk, k) = -X(kk, kk) T(kk, k)
+    for (int kk = 0; kk < nb; ++kk) {
+      DTask& t = B.add(1, {}, {xblk(j, kk, kk), xfin(j)});
+      t.kind = kLeafTask;
+      t.mode = 1;  // invert only: the input block (A-store slot of the sweep's table = L) is a factor block
+      t.c_off = t.c0_off = t.cm_off = blk_off(ds, bp, kk, kk);
+      t.diag_off = static_cast<long long>(j) * nb + kk;
+      t.m0 = valid - kk * kB;
+      t.n0 = static_cast<int>(static_cast<long>(j) * L.b + kk * kB);
+      if (kk + 1 < nb) P.zero.push_back(ZeroStrip{blk_off(ds, bp, kk, kk) + kB, nb - 1 - kk, 0});
+      P.task_flops += 2.0 * (kB * kB * kB / 6.0);
+    }
+    for (int kk = 1; kk < nb; ++kk)
+      for (int k = 0; k < kk; ++k) {
+        for (int l = k; l < kk; ++l) {
+          DTask& t = B.add(1, {{xblk(j, l, k), 1}, {tcnt(j, kk, k), l - k}}, {tcnt(j, kk, k)});
+          t.kind = kGemmTask;
+          t.c_store = kStoreScratch;
+          t.c_off = tsz * j + static_cast<long long>(kk) * kB * bp + k * kB;
+          if (l > k) {
+            t.c0_store = kStoreScratch;
+            t.c0_off = t.c_off;
+          }
+          B.seg(t, kStoreL, blk_off(ds, bp, kk, l), kStoreP1, blk_off(ds, bp, l, k), 0, kB, 0);
+        }
+        DTask& t = B.add(1, {{xblk(j, kk, kk), 1}, {tcnt(j, kk, k), kk - k}}, {xblk(j, kk, k), xfin(j)});
+        t.kind = kGemmTask;
+        t.c_store = kStoreP1;
+        t.c_off = blk_off(ds, bp, kk, k);
+        B.seg(t, kStoreP1, blk_off(ds, bp, kk, kk), kStoreScratch, tsz * j + static_cast<long long>(kk) * kB * bp + k * kB,
+              0, kB, kNegate);
+      }
+    // W_kj = L_kj X_j (trmm_tile(kRight, kTrans) by U_j^T, selinv.cpp:203-216)
+    for (const int* r = F.rows_begin(j); r != F.rows_end(j); ++r) {
+      if (*r <= j) continue;
+      const long sk = F.slot(*r, j);
+      for (int p = 0; p < nb; ++p)
+        for (int q = 0; q < nb; ++q) {
+          DTask& t = B.add(1, {{xfin(j), xdone}}, {wfin(sk)});
+          t.kind = kGemmTask;
+          t.c_store = kStoreP1;
+          t.c_off = blk_off(sk, bp, p, q);
+          t.m0 = p * kB;
+          t.n0 = q * kB;
+          B.seg(t, kStoreL, tile_off(sk, bp), kStoreP1, tile_off(ds, bp), q * kB, bp, 0);
+        }
+    }
+  }
+  B.finish(0);
+  return P;
+}
+
 DataflowPlan build_phase2_dataflow(const Pattern& F, const Closure& sel, int crit_workers) {
   DataflowPlan P;
   P.L = F.layout();

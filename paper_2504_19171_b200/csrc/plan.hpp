@@ -56,6 +56,12 @@ struct DataflowPlan {
 DataflowPlan build_factor_dataflow(const Pattern& filled, int crit_workers, int defer_w, bool fat_leaf,
                                    bool chain = false, bool boundary = false);
 
+// Phase 1 alone (selinv.cpp:195-237) from a given factor L (a factor read back
+// from a tile file): X_j = L_jj^{-1} and W_kj = L_kj X_j, every column
+// independent, all on the bulk queue.  The sweep's A-store entry must point at
+// the L store (the invert-only leaves read their block from there).
+DataflowPlan build_phase1_dataflow(const Pattern& filled);
+
 // Phase 2 over a closure: per column descending, off-diagonal targets split
 // into an early part and the k == j term, diagonal targets into LAUUM + early
 // terms and the first-row term; the first-row chain is queue 0.

@@ -190,6 +190,18 @@ struct HostMatrix {
 HostMatrix generate_arrowhead(long n, long w, long t, double density, uint64_t seed, int b);
 // Its tile pattern at density 1 (no values; the device generator fills them).
 Pattern arrowhead_pattern(long n, long w, long t, int b);
+// STLS tile files (tileio.cpp; reference tileio.cpp:30-94).  payload: per
+// pattern slot, b*b row-major.
+struct TileFileData {
+  Layout layout;
+  int phase = 0;  // PhaseTag: 0 matrix, 1 factor, 2 phase-1, 3 selected inverse
+  Pattern pattern;
+  std::vector<double> payload;
+};
+TileFileData read_tile_file(const std::string& path);
+void write_tile_file(const std::string& path, const Layout& layout, int phase, const Pattern& pattern,
+                     const double* payload);
+
 // BASELINE config 4: AR1(rho, nt) (x) SPDE(nx x ny lattice) latent field plus p
 // fixed effects, as the joint INLA precision (kronecker.cpp).
 HostMatrix generate_kronecker(int nt, int nx, int ny, int p, double rho, double kappa2, double tau, double tau_y,

@@ -24,6 +24,11 @@ this; it only reads the committed fixtures.
                   effects) at reduced scale through read_matrix_market_file
     python tests/golden/make_golden.py configs [DIR]   (DIR: reuse outputs of
     an earlier `ref_driver golden` run written as DIR/<name>.*)
+  stls/*.stls.gz  tile files the reference wrote itself (`ref_driver stls`:
+                  write_tile_file of the generated matrix, the factor, the
+                  phase-1 tiles, and write_selected_inverse of the pattern
+                  inverse) -- byte-compatibility fixtures of the STLS I/O
+    python tests/golden/make_golden.py stls
 """
 import json
 import os
@@ -126,7 +131,29 @@ def configs(from_dir=None):
             print("config", name, "logdet", info["logdet"])
 
 
+STLS_CASES = {"case_b32": (200, 30, 6, 32, 4), "case_b100": (250, 30, 6, 100, 3)}  # n, w, t, b, seed
+
+
+def stls():
+    import gzip
+    import shutil
+    out = os.path.join(HERE, "stls")
+    os.makedirs(out, exist_ok=True)
+    with tempfile.TemporaryDirectory() as tmp:
+        for name, (n, w, t, b, seed) in STLS_CASES.items():
+            subprocess.run([os.path.join(REF, "ref_driver"), "stls", str(n), str(w), str(t), str(b), str(seed),
+                            os.path.join(tmp, name)], check=True)
+            for kind in ("matrix", "factor", "phase1", "sigma"):
+                with open(os.path.join(tmp, f"{name}.{kind}.stls"), "rb") as fi, \
+                        gzip.GzipFile(os.path.join(out, f"{name}.{kind}.stls.gz"), "wb", compresslevel=9, mtime=0) as fo:
+                    shutil.copyfileobj(fi, fo)
+    print("stls fixtures:", sorted(os.listdir(out)))
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "stls":
+        stls()
+        return
     if len(sys.argv) > 1 and sys.argv[1] == "configs":
         configs(sys.argv[2] if len(sys.argv) > 2 else None)
         return
