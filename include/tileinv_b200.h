@@ -102,6 +102,21 @@ int tib_symbolic_closure(tib_matrix m, int preset, const long* rows, const long*
 int tib_flops(tib_matrix m, int preset, const long* rows, const long* cols, long nentries,
               double* factorize, double* phase1, double* phase2);
 
+/* ---- task-graph / complexity analyzer (dag.hpp:12-77, dag.cpp:79-342;
+ * Python dag_report / export_dot / predict_gemm_count, module.cpp:217-236) --
+ * report[9] = {n_tiles, band_b (-1: none), trsm, trmm, lauum, gemm_actual,
+ * gemm_predicted (-1: none), critical_path, match}.                          */
+/* count_kernels(build_band_arrow_dag(n_tiles, band > 0 ? band : n_tiles))   */
+int tib_dag_report(int n_tiles, int band, long long* report);
+/* count_kernels(build_dag(closure of the request, filled pattern of m))     */
+int tib_dag_report_matrix(tib_matrix m, int preset, const long* rows, const long* cols, long nentries,
+                          long long* report);
+/* export_dot(assign_cores(build_band_arrow_dag(...), cores) if cores > 0);
+ * *len_inout is the buffer size, on return the full text size.              */
+int tib_dag_export_dot(int n_tiles, int band, int cores, char* buf, size_t* len_inout);
+/* predict_gemm_count (dag.cpp:272-280)                                        */
+int tib_predict_gemm_count(int n_tiles, int band, long long* out);
+
 /* ---- factorization (cholesky.hpp:28-33, selinv.cpp:195-237) --------------- */
 /* symbolic_cholesky + factorize on `device`.  The factor stays in HBM; the
  * phase-1 transform (U_j, W_kj) is produced in the same column sweep.  On

@@ -499,6 +499,53 @@ def task_flops(matrix: Matrix, selection="pattern"):
     return f.value, p1.value, p2.value
 
 
+_REPORT_KEYS = ("n_tiles", "band_b", "trsm", "trmm", "lauum", "gemm_actual", "gemm_predicted", "critical_path",
+                "match")
+
+
+def _report_dict(v) -> dict:
+    """ComplexityReport -> dict with the reference's keys (module.cpp:109-121)."""
+    out = dict(zip(_REPORT_KEYS, (int(x) for x in v)))
+    out["band_b"] = None if out["band_b"] < 0 else out["band_b"]
+    out["gemm_predicted"] = None if out["gemm_predicted"] < 0 else out["gemm_predicted"]
+    out["match"] = bool(out["match"])
+    return out
+
+
+def dag_report(n_tiles: int, band: int = 0) -> dict:
+    """Kernel counts and critical path of the band+arrow inversion task graph
+    (count_kernels(build_band_arrow_dag(n_tiles, band or n_tiles)), module.cpp:217-223)."""
+    v = (C.c_longlong * 9)()
+    _check(lib.tib_dag_report(n_tiles, band, v))
+    return _report_dict(v)
+
+
+def dag_report_of(matrix: Matrix, selection="pattern") -> dict:
+    """The same report for a matrix's filled factor pattern and the closure of
+    `selection` (build_dag(symbolic_inversion(...), pattern), dag.cpp:79-190)."""
+    preset, rows, cols, ne = _request(selection)
+    v = (C.c_longlong * 9)()
+    _check(lib.tib_dag_report_matrix(matrix._h, preset, _lp(rows), _lp(cols), ne, v))
+    return _report_dict(v)
+
+
+def export_dot(n_tiles: int, band: int = 0, cores: int = 0) -> str:
+    """Canonical DOT text of the band+arrow task graph, nodes coloured by
+    owning core when cores > 0 (module.cpp:225-233, dag.cpp:247-270)."""
+    n = C.c_size_t(0)
+    _check(lib.tib_dag_export_dot(n_tiles, band, cores, None, C.byref(n)))
+    buf = C.create_string_buffer(n.value)
+    _check(lib.tib_dag_export_dot(n_tiles, band, cores, buf, C.byref(n)))
+    return buf.raw[: n.value].decode()
+
+
+def predict_gemm_count(n_tiles: int, band: int) -> int:
+    """Closed-form phase-2 GEMM count of the band+arrow recursion (dag.cpp:272-280)."""
+    v = C.c_longlong()
+    _check(lib.tib_predict_gemm_count(n_tiles, band, C.byref(v)))
+    return v.value
+
+
 def bench_resident(matrix: Matrix, reps: int, warmup: int, device: int = 0):
     """Device-resident timing of the fused sweep: (ms/rep, ms factor, ms phase2, logdet)."""
     a, b, c, d = C.c_double(), C.c_double(), C.c_double(), C.c_double()
@@ -517,7 +564,8 @@ __all__ = [
     "Factor", "Matrix", "NotSpdError", "SelectedInverseResult", "TileinvError", "__version__",
     "factorize", "from_dense", "from_tiles", "generate", "read_matrix_market", "selected_inverse",
     "selected_inverse_of_factor", "write_matrix_market", "selected_inverse_batch", "factor_pattern",
-    "closure_tiles", "task_flops", "bench_resident", "device_count",
+    "closure_tiles", "task_flops", "bench_resident", "device_count", "dag_report", "dag_report_of", "export_dot",
+    "predict_gemm_count",
 ]
 
 

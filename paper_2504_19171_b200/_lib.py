@@ -50,6 +50,10 @@ SIGNATURES = {
     "tib_symbolic_pattern": [_p, _pl, _pi, _pi],
     "tib_symbolic_closure": [_p, _i, _pl, _pl, _l, _pl, _pi, _pi, _pi],
     "tib_flops": [_p, _i, _pl, _pl, _l, _pd, _pd, _pd],
+    "tib_dag_report": [_i, _i, C.POINTER(C.c_longlong)],
+    "tib_dag_report_matrix": [_p, _i, _pl, _pl, _l, C.POINTER(C.c_longlong)],
+    "tib_dag_export_dot": [_i, _i, _i, C.c_char_p, C.POINTER(C.c_size_t)],
+    "tib_predict_gemm_count": [_i, _i, C.POINTER(C.c_longlong)],
     "tib_factorize": [_p, _i, _pp],
     "tib_factor_info": [_p, _pl, _pi, _pl],
     "tib_factor_logdet": [_p, _pd],

@@ -1176,6 +1176,36 @@ int tib_flops(tib_matrix m, int preset, const long* rows, const long* cols, long
   });
 }
 
+static void put_report(const KernelReport& r, long long* out) {
+  const long long v[9] = {r.n_tiles, r.band_b, r.trsm, r.trmm, r.lauum, r.gemm_actual, r.gemm_predicted,
+                          r.critical_path, r.match ? 1 : 0};
+  std::memcpy(out, v, sizeof(v));
+}
+int tib_dag_report(int n_tiles, int band, long long* report) {
+  return guarded([&] { put_report(count_task_kernels(band_arrow_task_graph(n_tiles, band > 0 ? band : n_tiles)), report); });
+}
+int tib_dag_report_matrix(tib_matrix m, int preset, const long* rows, const long* cols, long ne, long long* report) {
+  return guarded([&] {
+    need(m, "matrix");
+    const FactorPlan plan = symbolic_cholesky(m->pattern);
+    const Closure c = symbolic_inversion(select_tiles(plan.filled.layout(), plan.filled, make_request(preset, rows, cols, ne)),
+                                         plan.filled);
+    put_report(count_task_kernels(build_task_graph(c, plan.filled)), report);
+  });
+}
+int tib_dag_export_dot(int n_tiles, int band, int cores, char* buf, size_t* len) {
+  return guarded([&] {
+    TaskGraph g = band_arrow_task_graph(n_tiles, band > 0 ? band : n_tiles);
+    if (cores > 0) assign_task_cores(g, cores);
+    const std::string text = task_graph_dot(g);
+    if (buf && *len >= text.size()) std::memcpy(buf, text.data(), text.size());
+    *len = text.size();
+  });
+}
+int tib_predict_gemm_count(int n_tiles, int band, long long* out) {
+  return guarded([&] { *out = predict_gemm_count(n_tiles, band); });
+}
+
 int tib_factorize(tib_matrix m, int device, tib_factor* out) {
   return guarded([&] {
     need(m, "matrix");

@@ -15,6 +15,7 @@
 //   symbolic_inversion    <- proj/src/selinv.cpp:85-150
 //   extract (entry order) <- extract_entries, proj/src/selinv.cpp:387-439
 //   payload_checksum      <- proj/src/storage.cpp:34-48
+//   task graph analyzer   <- proj/src/dag.cpp:79-342 (dag.cpp)
 //
 // Numeric payloads never live here: the device store (store.cuh) owns them.
 #pragma once
@@ -164,6 +165,34 @@ void for_each_request_entry(const Layout& L, const Pattern& closure,
                             const std::vector<Coord>& requested, const Request& req, F&& visit);
 
 uint64_t fnv1a_keys(const std::vector<Coord>& tiles);
+
+// ---- task-graph / complexity analyzer (dag.cpp; reference dag.hpp:12-77) ------
+struct DagNode {
+  int kind = 0;  // 0 TRSM_INV, 1 TRMM, 2 LAUUM, 3 GEMM (the reference's rank order)
+  int i = 0, j = 0;
+  int k = -1;    // accumulation term of a GEMM
+  int phase = 1;
+};
+struct TaskGraph {
+  int n_tiles = 0;
+  int band_b = -1;  // band width when closure == factor == band+arrow, else -1
+  std::vector<DagNode> nodes;  // canonical order; ids are indices
+  std::vector<std::pair<int, int>> edges;
+  std::vector<int> core_of;    // empty until assign_task_cores
+};
+struct KernelReport {
+  int n_tiles = 0, band_b = -1, critical_path = 0;
+  long long trsm = 0, trmm = 0, lauum = 0, gemm_actual = 0, gemm_predicted = -1;
+  bool match = false;
+};
+TaskGraph build_task_graph(const Closure& sel, const Pattern& factor);
+TaskGraph band_arrow_task_graph(int n_tiles, int band_b);
+void assign_task_cores(TaskGraph& g, int cores);
+int task_graph_critical_path(const TaskGraph& g);
+std::string task_graph_dot(const TaskGraph& g);
+long long predict_gemm_count(int n_tiles, int band_b);
+KernelReport count_task_kernels(const TaskGraph& g);
+
 
 // FNV-1a over (tile key, b*b payload) in column-major tile order.
 struct Fnv {

@@ -29,6 +29,10 @@ this; it only reads the committed fixtures.
                   phase-1 tiles, and write_selected_inverse of the pattern
                   inverse) -- byte-compatibility fixtures of the STLS I/O
     python tests/golden/make_golden.py stls
+  dag.json        the reference's task-graph analyzer (dag_report, export_dot,
+                  predict_gemm_count of module.cpp:217-236) over small band+arrow
+                  grids: reports, DOT text (plain and core-coloured), closed forms
+    python tests/golden/make_golden.py dag
 """
 import json
 import os
@@ -150,7 +154,29 @@ def stls():
     print("stls fixtures:", sorted(os.listdir(out)))
 
 
+DAG_GRIDS = [(n, b) for n in range(1, 11) for b in range(0, n + 1)] + [(24, 3), (40, 5), (61, 7)]
+
+
+def dag():
+    out = {"reports": [], "dots": [], "predict": []}
+    for n, b in DAG_GRIDS:
+        out["reports"].append([n, b, R.dag_report(n, b)])
+    for n, b in DAG_GRIDS:
+        if n <= 7:
+            for cores in (0, 3, 9):
+                out["dots"].append([n, b, cores, R.export_dot(n, b, cores)])
+    for n in (1, 2, 7, 391, 1000, 4096):
+        for b in sorted({1, 2, 5, min(n, 11), n}):
+            if b <= n:
+                out["predict"].append([n, b, R.predict_gemm_count(n, b)])
+    with open(os.path.join(HERE, "dag.json"), "w") as f:
+        json.dump(out, f)
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "dag":
+        dag()
+        return
     if len(sys.argv) > 1 and sys.argv[1] == "stls":
         stls()
         return
