@@ -442,6 +442,7 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
   // the chains' workers are reserved ones (worker 0 of the first CTAs): keep
   // the plan's count of reserved workers for the chain's helpers
   if (a.static_chains) a.q0.workers += batch;
+  a.agent = a.dedicate && a.static_chains && env_int("TIB_AGENT", 1) ? 1 : 0;
   a.poll_uploads = poll ? 1 : 0;
   a.watchdog_ns = static_cast<unsigned long long>(env_int("TIB_WATCHDOG_S", 60)) * 1000000000ull;
   a.slots0 = a.missing + nt * batch;

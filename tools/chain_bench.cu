@@ -20,6 +20,7 @@ __global__ void chain_kernel(const double* A, const double* P, const double* Dn,
       __syncthreads();
     }
     const long long t0 = clock64();
+    PROF(-1);
     if (mode == 4) {
       // the sweep's pipelining: the previous step's D' tail on warps 2-3 during
       // the first 32x32 sweep (operands: whatever SP / SA hold)
@@ -37,9 +38,11 @@ __global__ void chain_kernel(const double* A, const double* P, const double* Dn,
       for (int idx = threadIdx.x; idx < kL2 * kL2; idx += kGemmThreads) SX[(idx / kL2) * kLs + kL2 + (idx % kL2)] = 0.0;
       cp_async_wait<0>();
       __syncthreads();
+      PROF(6);
       fat_t0 = clock64();
       chain_fat_head(Pout, 64, smem);
       fat_t += clock64() - fat_t0;
+      PROF(7);
       if (threadIdx.x >= 64) chain_fat_tail(smem);
       __syncthreads();
     }
@@ -82,12 +85,27 @@ int main() {
   cudaMemcpy(dP, p.data(), 32768, cudaMemcpyHostToDevice);
   cudaMemset(st, 0xff, 8);
   cudaFuncSetAttribute(chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFlowSmemBytes);
+#ifdef TIB_PROF
+  long long* prof;
+  cudaMalloc(&prof, 16 * 8);
+  cudaMemcpyToSymbol(g_prof, &prof, sizeof(prof));
+#endif
   for (int mode : {0, 1, 2, 4, 0, 1, 2, 4}) {
+#ifdef TIB_PROF
+    cudaMemset(prof, 0, 16 * 8);
+#endif
     chain_kernel<<<1, 128, kFlowSmemBytes>>>(dA, dP, dA, dL, dX, dPo, st, dld, cyc, 50, mode);
     long long c[3];
     cudaMemcpy(c, cyc, 24, cudaMemcpyDeviceToHost);
     printf("{\"mode\": %d, \"step_cycles\": %lld, \"leaf_cycles\": %lld, \"fat_dmma_cycles\": %lld, \"err\": \"%s\"}\n", mode, c[0], c[1], c[2],
            cudaGetErrorString(cudaGetLastError()));
+#ifdef TIB_PROF
+    long long h[16];
+    cudaMemcpy(h, prof, 16 * 8, cudaMemcpyDeviceToHost);
+    printf("  prof per step:");
+    for (int i = 0; i < 10; ++i) printf(" p%d=%lld", i, h[i] / 50);
+    printf("\n");
+#endif
   }
   return 0;
 }
