@@ -278,6 +278,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="large", choices=sorted(CONFIGS))
     ap.add_argument("--batch-count", type=int, default=None, help="matrices of the batch config (default 64)")
+    ap.add_argument("--tile", type=int, default=None, help="tile size b (default: the config's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-full", action="store_true", help="reference arm: the whole workload, one run")
     ap.add_argument("--ref-workers1", action="store_true", help="reference arm: also a workers=1 run")
@@ -320,6 +321,7 @@ def main():
     import paper_2504_19171_b200 as tib
 
     n, w, t, b = CONFIGS[args.config]
+    b = args.tile or b
     total = args.batch_count or BATCH_TOTAL.get(args.config)
     if total:
         seeds = batch_seeds(1000, total, rank, world)

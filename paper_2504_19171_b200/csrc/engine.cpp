@@ -442,6 +442,7 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
   // the chains' workers are reserved ones (worker 0 of the first CTAs): keep
   // the plan's count of reserved workers for the chain's helpers
   if (a.static_chains) a.q0.workers += batch;
+  a.poll_shift = env_int("TIB_POLL_SHIFT", 0);
   a.agent = a.dedicate && a.static_chains && env_int("TIB_AGENT", 1) ? 1 : 0;
   a.poll_uploads = poll ? 1 : 0;
   a.watchdog_ns = static_cast<unsigned long long>(env_int("TIB_WATCHDOG_S", 60)) * 1000000000ull;
@@ -827,7 +828,7 @@ static SigmaObj* selected_inverse_matrix(const MatrixObj& m, const Request& req,
   res->var = DevBuf(static_cast<size_t>(m.layout.N) * fp->bp, device, s);
   std::vector<BaseTable> tables{make_table(st.A.p, st.L.p, st.P1.p, res->S.p, res->var.p, st.scratch.p, st.logdet.p, st.status.p, st.ctr(0))};
   if (stream_up) {
-    cudaEvent_t cleared, uploaded;
+    cudaEvent_t cleared, uploaded, t_start = nullptr, t_up = nullptr, t_sweep = nullptr;
     CK(cudaEventCreateWithFlags(&cleared, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&uploaded, cudaEventDisableTiming));
     const size_t bb = static_cast<size_t>(fp->bp) * fp->bp;
@@ -847,8 +848,25 @@ static SigmaObj* selected_inverse_matrix(const MatrixObj& m, const Request& req,
         CK(cudaMemcpyAsync(upl + c, rt.one, sizeof(int), cudaMemcpyHostToDevice, rt.upload));
       }
       CK(cudaEventRecord(uploaded, rt.upload));
+      if (tm.on) CK(cudaEventRecord(t_up, rt.upload));
     };
+    if (tm.on) {
+      CK(cudaEventCreate(&t_start));
+      CK(cudaEventCreate(&t_up));
+      CK(cudaEventCreate(&t_sweep));
+      CK(cudaEventRecord(t_start, s));
+    }
     factor_sweep(*fp, st, s, tables, &up);
+    if (tm.on) {
+      CK(cudaEventRecord(t_sweep, s));
+      CK(cudaEventSynchronize(t_sweep));
+      CK(cudaEventSynchronize(t_up));
+      float u = 0, w = 0;
+      cudaEventElapsedTime(&u, t_start, t_up);
+      cudaEventElapsedTime(&w, t_start, t_sweep);
+      std::fprintf(stderr, "[tib timing] streamed upload done at %.3f ms, factor sweep at %.3f ms (%.1f GB/s)\n", u, w,
+                   static_cast<double>(F.size()) * bb * 8 / (u * 1e6));
+    }
     CK(cudaStreamWaitEvent(s, uploaded, 0));
     cudaEventDestroy(cleared);
     cudaEventDestroy(uploaded);
@@ -1496,18 +1514,51 @@ int tib_selected_inverse_batch(const tib_matrix* ms, int count, int device, doub
     // streamed upload (as the single path): tile column c of every matrix goes
     // up on the copy stream, column-major over the batch, while the batched
     // factor sweep runs; each matrix's tasks poll that matrix's column counters
-    bool stream_up = fp->bp == m0.layout.b && env_int("TIB_STREAM_UPLOAD", 1) != 0 && fp->flow->host.upl >= 0 &&
+    bool host_ready = fp->bp == m0.layout.b;
+    for (int k = 0; k < count; ++k) host_ready = host_ready && !ms[k]->gen.on && ms[k]->payload.pinned;
+    // pipelined batch: groups of `pipe` matrices, each group's upload (one
+    // copy per matrix on the copy stream) overlapping the previous group's
+    // two sweeps.  A batch streamed column-wise under one launch stalls: with
+    // tens of matrices every worker ends up waiting in a task whose target
+    // column has not arrived, and the sweep runs after the upload, not under it.
+    const int pipe = env_int("TIB_BATCH_PIPE", 16);
+    const bool pipelined = host_ready && F == m0.pattern && pipe > 0 && count > pipe;
+    bool stream_up = !pipelined && host_ready && env_int("TIB_STREAM_UPLOAD", 1) != 0 && fp->flow->host.upl >= 0 &&
                      static_cast<size_t>(count) <= max_batch(*fp->flow);
-    for (int k = 0; k < count; ++k) stream_up = stream_up && !ms[k]->gen.on && ms[k]->payload.pinned;
     for (int k = 0; k < count; ++k) {
-      if (!stream_up) upload_matrix(*ms[k], F, fp->bp, st.A.p + T * tile * k, s);
+      if (!stream_up && !pipelined) upload_matrix(*ms[k], F, fp->bp, st.A.p + T * tile * k, s);
       tables.push_back(make_table(st.A.p + T * tile * k, st.L.p + T * tile * k, st.P1.p + T * tile * k,
                                   Sg.p + p2->sel.closure.size() * tile * k, var.p + static_cast<size_t>(m0.layout.N) * fp->bp * k,
                                   st.scratch.p + st.scratch_stride * k,
                                   st.logdet.p + fp->flow->host.logdet_doubles * k, st.status.p + k, st.ctr(k)));
     }
-    if (stream_up) {
-      cudaEvent_t cleared, uploaded;
+    if (pipelined) {
+      CK(cudaMemsetAsync(st.status.p, 0xff, static_cast<size_t>(count) * sizeof(unsigned long long), s));
+      std::vector<cudaEvent_t> evs;
+      cudaEvent_t ready;
+      CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+      CK(cudaEventRecord(ready, s));  // the stores are allocated (stream-ordered) before the copies
+      CK(cudaStreamWaitEvent(rt.upload, ready, 0));
+      evs.push_back(ready);
+      for (int c0 = 0; c0 < count; c0 += pipe) {
+        const int c1 = std::min(count, c0 + pipe);
+        for (int k = c0; k < c1; ++k)
+          CK(cudaMemcpyAsync(st.A.p + T * tile * k, ms[k]->payload.p, T * tile * sizeof(double), cudaMemcpyHostToDevice,
+                             rt.upload));
+        cudaEvent_t ev;
+        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CK(cudaEventRecord(ev, rt.upload));
+        CK(cudaStreamWaitEvent(s, ev, 0));
+        evs.push_back(ev);
+        const std::vector<BaseTable> part(tables.begin() + c0, tables.begin() + c1);
+        run_flow_chunked(*fp->flow, part, s);
+        run_flow_chunked(*p2->flow, part, s);
+      }
+      tm.mark("pipelined sweeps");
+      CK(cudaStreamSynchronize(s));
+      for (cudaEvent_t e : evs) cudaEventDestroy(e);
+    } else if (stream_up) {
+      cudaEvent_t cleared, uploaded, t_start = nullptr, t_up = nullptr, t_sweep = nullptr;
       CK(cudaEventCreateWithFlags(&cleared, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&uploaded, cudaEventDisableTiming));
       const bool same = F == m0.pattern;
@@ -1534,8 +1585,25 @@ int tib_selected_inverse_batch(const tib_matrix* ms, int count, int device, doub
                                static_cast<size_t>(ce - c) * sizeof(int), cudaMemcpyHostToDevice, rt.upload));
           }
         CK(cudaEventRecord(uploaded, rt.upload));
+        if (tm.on) CK(cudaEventRecord(t_up, rt.upload));
       };
+      if (tm.on) {
+        CK(cudaEventCreate(&t_start));
+        CK(cudaEventCreate(&t_up));
+        CK(cudaEventCreate(&t_sweep));
+        CK(cudaEventRecord(t_start, s));
+      }
       factor_sweep(*fp, st, s, tables, &up);
+      if (tm.on) {
+        CK(cudaEventRecord(t_sweep, s));
+        CK(cudaEventSynchronize(t_sweep));
+        CK(cudaEventSynchronize(t_up));
+        float u = 0, w = 0;
+        cudaEventElapsedTime(&u, t_start, t_up);
+        cudaEventElapsedTime(&w, t_start, t_sweep);
+        std::fprintf(stderr, "[tib timing] streamed upload done at %.3f ms, factor sweep at %.3f ms (%.1f GB/s)\n", u, w,
+                     static_cast<double>(T) * tile * count * 8 / (u * 1e6));
+      }
       CK(cudaStreamWaitEvent(s, uploaded, 0));
       cudaEventDestroy(cleared);
       cudaEventDestroy(uploaded);
@@ -1543,9 +1611,11 @@ int tib_selected_inverse_batch(const tib_matrix* ms, int count, int device, doub
       tm.mark("uploads");
       factor_sweep(*fp, st, s, tables);
     }
-    tm.mark("factor sweep");
-    phase2_sweep(*p2, s, tables);
-    tm.mark("phase-2 sweep");
+    if (!pipelined) {
+      tm.mark("factor sweep");
+      phase2_sweep(*p2, s, tables);
+      tm.mark("phase-2 sweep");
+    }
     std::vector<double> parts(static_cast<size_t>(m0.layout.N) * fp->nb * count);
     std::vector<double> v(var.n);
     CK(cudaMemcpyAsync(parts.data(), st.logdet.p, parts.size() * sizeof(double), cudaMemcpyDeviceToHost, s));

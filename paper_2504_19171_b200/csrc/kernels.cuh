@@ -36,6 +36,7 @@ struct FlowArgs {
   const DTask* chain;  // chain steps (kChainTask)
   int dedicate;        // chains get their SM to themselves
   int static_chains;   // chains run on worker 0 of CTAs 0 .. batch-1 (q0 items 0 .. batch-1 skipped)
+  int poll_shift;      // polling backoff caps scaled by 2^poll_shift
   int agent;           // with dedicate + static_chains: the chain's sibling worker raises its signals
   int poll_uploads;    // streamed upload: tasks wait for their A-store column (DTask::poll)
   unsigned long long watchdog_ns;  // a spin longer than this aborts the sweep (TIB_ERR_CUDA)
