@@ -408,7 +408,7 @@ static void write_trace(DevPlan& P, int batch, unsigned long long* d_trace, cuda
 // pre_launch (streamed upload): issued after the counters are cleared and
 // before the sweep kernel; tasks then poll their A-store column's counter.
 static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStream_t s,
-                     const std::function<void()>* pre_launch = nullptr) {
+                     const std::function<void()>* pre_launch = nullptr, cudaEvent_t cleared = nullptr) {
   std::lock_guard<std::mutex> lk(P.mu);
   const int batch = static_cast<int>(tables.size());
   const size_t nt = P.host.tasks.size();
@@ -417,7 +417,13 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
   CK(cudaMemcpyAsync(e.tables, tables.data(), sizeof(BaseTable) * batch, cudaMemcpyHostToDevice, s));
   for (const BaseTable& t : tables)
     CK(cudaMemsetAsync(t.p[kStoreCounters], 0, static_cast<size_t>(P.host.counters) * sizeof(int), s));
-  if (pre_launch) (*pre_launch)();
+  if (cleared) CK(cudaEventRecord(cleared, s));  // the copy stream's counter writes come after this
+  // streamed upload: the copies are enqueued on the copy stream once the sweep
+  // is launched (its tasks poll the column counters), so the host's issue of
+  // thousands of copies overlaps the sweep instead of delaying its launch
+  auto launched = [&]() {
+    if (pre_launch) (*pre_launch)();
+  };
   FlowArgs a{};
   a.tasks = P.tasks.p;
   a.segs = P.segs.p;
@@ -463,6 +469,7 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
     CK(static_cast<cudaError_t>(set_chain_profile(prof)));
     enqueue();
     CK(cudaGetLastError());
+    launched();
     long long h[16];
     CK(cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -482,6 +489,7 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
     a.trace = d_trace;
     enqueue();
     CK(cudaGetLastError());
+    launched();
     write_trace(P, batch, d_trace, s);
     CK(cudaFreeAsync(d_trace, s));
     return;
@@ -489,6 +497,7 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
   if (!use_graphs()) {
     enqueue();
     CK(cudaGetLastError());
+    launched();
     return;
   }
   if (!e.exec) {
@@ -502,6 +511,7 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
     cudaGraphDestroy(g);
   }
   CK(cudaGraphLaunch(e.exec, s));
+  launched();
 }
 
 // Largest batch one launch may carry: every chain needs its own CTA (static
@@ -515,10 +525,10 @@ static size_t max_batch(const DevPlan& P) {
 }
 
 static void run_flow_chunked(DevPlan& P, const std::vector<BaseTable>& tables, cudaStream_t s,
-                             const std::function<void()>* pre_launch = nullptr) {
+                             const std::function<void()>* pre_launch = nullptr, cudaEvent_t cleared = nullptr) {
   const size_t mb = max_batch(P);
   if (tables.size() <= mb) {
-    run_flow(P, tables, s, pre_launch);
+    run_flow(P, tables, s, pre_launch, cleared);
     return;
   }
   if (pre_launch) throw Error(kErrInvalidArgument, "streamed upload is single-launch only");
@@ -760,9 +770,9 @@ static double reduce_logdet(const double* parts, int N, int nb) {
 
 // Runs the fused factor sweep for the matrices already resident in their A stores.
 static void factor_sweep(FactorPlan2& P, SweepStores& st, cudaStream_t s, const std::vector<BaseTable>& tables,
-                         const std::function<void()>* pre_launch = nullptr) {
+                         const std::function<void()>* pre_launch = nullptr, cudaEvent_t cleared = nullptr) {
   CK(cudaMemsetAsync(st.status.p, 0xff, tables.size() * sizeof(unsigned long long), s));
-  run_flow_chunked(*P.flow, tables, s, pre_launch);
+  run_flow_chunked(*P.flow, tables, s, pre_launch, cleared);
 }
 
 static void phase2_sweep(Phase2Plan& P, cudaStream_t s, const std::vector<BaseTable>& tables) {
@@ -833,10 +843,12 @@ static SigmaObj* selected_inverse_matrix(const MatrixObj& m, const Request& req,
     CK(cudaEventCreateWithFlags(&uploaded, cudaEventDisableTiming));
     const size_t bb = static_cast<size_t>(fp->bp) * fp->bp;
     int* upl = reinterpret_cast<int*>(st.ctr(0)) + fp->flow->host.upl;
+    const bool same = F == m.pattern;
+    // fill-in slots are zero: one memset of the store on the sweep stream
+    // (a kernel cannot run beside the persistent sweep), then the copies
+    if (!same) CK(cudaMemsetAsync(st.A.p, 0, F.size() * bb * sizeof(double), s));
     std::function<void()> up = [&]() {
-      const bool same = F == m.pattern;
-      if (!same) upload_columns(m, F, 0, m.layout.N, st.A.p, s, false, true);
-      CK(cudaEventRecord(cleared, s));
+      const auto h0 = std::chrono::steady_clock::now();
       CK(cudaStreamWaitEvent(rt.upload, cleared, 0));
       for (int c = 0; c < m.layout.N; ++c) {
         const size_t t0 = static_cast<size_t>(F.col_start(c)), t1 = static_cast<size_t>(F.col_start(c + 1));
@@ -848,7 +860,11 @@ static SigmaObj* selected_inverse_matrix(const MatrixObj& m, const Request& req,
         CK(cudaMemcpyAsync(upl + c, rt.one, sizeof(int), cudaMemcpyHostToDevice, rt.upload));
       }
       CK(cudaEventRecord(uploaded, rt.upload));
-      if (tm.on) CK(cudaEventRecord(t_up, rt.upload));
+      if (tm.on) {
+        CK(cudaEventRecord(t_up, rt.upload));
+        std::fprintf(stderr, "[tib timing] copies enqueued in %.3f ms (host)\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
+      }
     };
     if (tm.on) {
       CK(cudaEventCreate(&t_start));
@@ -856,7 +872,7 @@ static SigmaObj* selected_inverse_matrix(const MatrixObj& m, const Request& req,
       CK(cudaEventCreate(&t_sweep));
       CK(cudaEventRecord(t_start, s));
     }
-    factor_sweep(*fp, st, s, tables, &up);
+    factor_sweep(*fp, st, s, tables, &up, cleared);
     if (tm.on) {
       CK(cudaEventRecord(t_sweep, s));
       CK(cudaEventSynchronize(t_sweep));
@@ -1566,10 +1582,8 @@ int tib_selected_inverse_batch(const tib_matrix* ms, int count, int device, doub
       // the copy engine needs time for, while each chain waits for little more
       // than its first group
       const int N = m0.layout.N, grp = std::max(1, std::min(kOnes, (N + 47) / 48));
+      if (!same) CK(cudaMemsetAsync(st.A.p, 0, T * tile * count * sizeof(double), s));
       std::function<void()> up = [&]() {
-        if (!same)
-          for (int k = 0; k < count; ++k) upload_columns(*ms[k], F, 0, N, st.A.p + T * tile * k, s, false, true);
-        CK(cudaEventRecord(cleared, s));
         CK(cudaStreamWaitEvent(rt.upload, cleared, 0));
         for (int c = 0; c < N; c += grp)
           for (int k = 0; k < count; ++k) {
@@ -1593,7 +1607,7 @@ int tib_selected_inverse_batch(const tib_matrix* ms, int count, int device, doub
         CK(cudaEventCreate(&t_sweep));
         CK(cudaEventRecord(t_start, s));
       }
-      factor_sweep(*fp, st, s, tables, &up);
+      factor_sweep(*fp, st, s, tables, &up, cleared);
       if (tm.on) {
         CK(cudaEventRecord(t_sweep, s));
         CK(cudaEventSynchronize(t_sweep));
