@@ -123,6 +123,14 @@ int tib_predict_gemm_count(int n_tiles, int band, long long* out);
  * TIB_ERR_NOT_SPD, tib_last_not_spd() carries the global pivot and tile.      */
 int tib_factorize(tib_matrix m, int device, tib_factor* out);
 int tib_factor_info(tib_factor f, long* n, int* tile_size, long* stored_tiles);
+/* Tiles (ti[k], tj[k]) of the factor L, b x b row-major each (host).        */
+int tib_factor_get_tiles(tib_factor f, long count, const int* ti, const int* tj, double* payload);
+/* Overwrites tiles of L in the device store and recomputes the phase-1
+ * transform and the log-determinant: the factor of a matrix that differs from
+ * the factored one only in a trailing block (the partitioned single-matrix
+ * path: the border block of a rank's local system).  No
+ * reference counterpart (the reference has no partitioned mode).           */
+int tib_factor_replace_tiles(tib_factor f, long count, const int* ti, const int* tj, const double* payload);
 /* 2 * sum_r log L_rr (not a reference API).               */
 int tib_factor_logdet(tib_factor f, double* out);
 /* Download L (phase = 1) or the phase-1 tiles U/W (phase = 2), column-major

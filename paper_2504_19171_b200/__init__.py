@@ -210,6 +210,33 @@ class Factor:
                                     pay.ctypes.data_as(C.POINTER(C.c_double))))
         return ti, tj, pay
 
+    def get_tiles(self, coords) -> np.ndarray:
+        """The L tiles at `coords` [(i, j), ...] as a (k, b, b) array."""
+        ti, tj = _coords(coords)
+        b = self.tile_size
+        pay = np.empty((len(ti), b, b), np.float64)
+        _check(lib.tib_factor_get_tiles(self._h, len(ti), ti.ctypes.data_as(C.POINTER(C.c_int)),
+                                        tj.ctypes.data_as(C.POINTER(C.c_int)),
+                                        pay.ctypes.data_as(C.POINTER(C.c_double))))
+        return pay
+
+    def replace_tiles(self, coords, payload) -> None:
+        """Overwrites L tiles on the device and recomputes the phase-1 tiles and
+        logdet (the partitioned path: the border block of a rank's system)."""
+        ti, tj = _coords(coords)
+        pay = np.ascontiguousarray(payload, np.float64)
+        b = self.tile_size
+        if pay.shape != (len(ti), b, b):
+            raise ValueError(f"payload shape {pay.shape} != {(len(ti), b, b)}")
+        _check(lib.tib_factor_replace_tiles(self._h, len(ti), ti.ctypes.data_as(C.POINTER(C.c_int)),
+                                            tj.ctypes.data_as(C.POINTER(C.c_int)),
+                                            pay.ctypes.data_as(C.POINTER(C.c_double))))
+
+
+def _coords(coords):
+    c = np.asarray(coords, np.int32).reshape(-1, 2)
+    return np.ascontiguousarray(c[:, 0]), np.ascontiguousarray(c[:, 1])
+
 
 class SelectedInverseResult:
     """SelectedInverse (selinv.hpp:61-68) + its request; device resident."""

@@ -57,6 +57,8 @@ SIGNATURES = {
     "tib_factorize": [_p, _i, _pp],
     "tib_factor_info": [_p, _pl, _pi, _pl],
     "tib_factor_logdet": [_p, _pd],
+    "tib_factor_get_tiles": [_p, _l, _pi, _pi, _pd],
+    "tib_factor_replace_tiles": [_p, _l, _pi, _pi, _pd],
     "tib_factor_tiles": [_p, _i, _pi, _pi, _pd],
     "tib_factor_checksum": [_p, _pu64],
     "tib_factor_free": [_p],

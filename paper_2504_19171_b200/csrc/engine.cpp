@@ -972,6 +972,46 @@ static void upload_host_tiles(const Pattern& F, int b, int bp, const double* pay
   CK(cudaStreamSynchronize(s));
 }
 
+// The phase-1 transform (X_j = L_jj^{-1}, W_kj = L_kj X_j) of a factor's L
+// store on the device (build_phase1_dataflow; selinv.cpp:195-223).
+static void run_phase1(FactorObj& f) {
+  DeviceRt& rt = runtime(f.device);
+  cudaStream_t s = rt.stream;
+  auto plan = phase1_plan_for(f.F, f.device, s);
+  DevBuf scratch(plan->host.scratch_doubles, f.device, s);
+  DevBuf logdet(plan->host.logdet_doubles, f.device, s);
+  DevBuf status(1, f.device, s);
+  CK(cudaMemsetAsync(status.p, 0xff, sizeof(unsigned long long), s));
+  DevBuf ctr = alloc_counters(plan->host.counters, 1, f.device, s);
+  // the invert-only leaves read their block through the A-store entry: L
+  std::vector<BaseTable> tables{make_table(f.L.p, f.L.p, f.P1.p, nullptr, nullptr, scratch.p, logdet.p, status.p, ctr.p)};
+  run_flow_chunked(*plan, tables, s);
+  CK(cudaStreamSynchronize(s));
+  check_watchdog();
+}
+
+// Tiles (i, j) of a factor store <-> host b x b row-major payloads.
+static void factor_tile_copy(FactorObj& f, const DevBuf& store, long count, const int* ti, const int* tj, double* host,
+                             bool to_device) {
+  DeviceRt& rt = runtime(f.device);
+  const int b = f.layout.b;
+  const size_t bpp = static_cast<size_t>(f.bp) * f.bp, bb = static_cast<size_t>(b) * b;
+  for (long k = 0; k < count; ++k) {
+    const long slot = f.F.slot(ti[k], tj[k]);
+    if (slot < 0)
+      throw Error(kErrContract, "tile (" + std::to_string(ti[k]) + ", " + std::to_string(tj[k]) + ") is not in the factor");
+    double* d = store.p + static_cast<size_t>(slot) * bpp;
+    double* h = host + static_cast<size_t>(k) * bb;
+    if (to_device)
+      CK(cudaMemcpy2DAsync(d, f.bp * sizeof(double), h, b * sizeof(double), b * sizeof(double), b,
+                           cudaMemcpyHostToDevice, rt.stream));
+    else
+      CK(cudaMemcpy2DAsync(h, b * sizeof(double), d, f.bp * sizeof(double), b * sizeof(double), b,
+                           cudaMemcpyDeviceToHost, rt.stream));
+  }
+  CK(cudaStreamSynchronize(rt.stream));
+}
+
 // A factor from host tiles (factor_from_tile_file, tileio.cpp:109-117): phase 1
 // = the factor L (phase 1 then runs on the device: build_phase1_dataflow),
 // phase 2 = phase-1 tiles U / W (used as they are; selinv.cpp:355 skips
@@ -1005,17 +1045,7 @@ static FactorObj* factor_from_host(const Layout& L, int phase, const Pattern& P,
   }
   f->L = DevBuf(P.size() * tile, device, s);
   upload_host_tiles(P, L.b, f->bp, pay, f->L.p, s, false);
-  auto plan = phase1_plan_for(P, device, s);
-  DevBuf scratch(plan->host.scratch_doubles, device, s);
-  DevBuf logdet(plan->host.logdet_doubles, device, s);
-  DevBuf status(1, device, s);
-  CK(cudaMemsetAsync(status.p, 0xff, sizeof(unsigned long long), s));
-  DevBuf ctr = alloc_counters(plan->host.counters, 1, device, s);
-  // the invert-only leaves read their block through the A-store entry: L
-  std::vector<BaseTable> tables{make_table(f->L.p, f->L.p, f->P1.p, nullptr, nullptr, scratch.p, logdet.p, status.p, ctr.p)};
-  run_flow_chunked(*plan, tables, s);
-  CK(cudaStreamSynchronize(s));
-  check_watchdog();
+  run_phase1(*f);
   return f.release();
 }
 
@@ -1273,6 +1303,40 @@ int tib_factor_info(tib_factor f, long* n, int* b, long* stored) {
     if (n) *n = f->layout.n;
     if (b) *b = f->layout.b;
     if (stored) *stored = static_cast<long>(f->F.size());
+  });
+}
+int tib_factor_get_tiles(tib_factor f, long count, const int* ti, const int* tj, double* payload) {
+  return guarded([&] {
+    need(f, "factor");
+    if (!f->has_L) throw Error(kErrContract, "the factor holds phase-1 tiles only (kPhase1 input)");
+    if (count < 0 || (count > 0 && (!ti || !tj || !payload))) throw Error(kErrInvalidArgument, "null tile arrays");
+    factor_tile_copy(*f, f->L, count, ti, tj, payload, false);
+  });
+}
+int tib_factor_replace_tiles(tib_factor f, long count, const int* ti, const int* tj, const double* payload) {
+  return guarded([&] {
+    need(f, "factor");
+    if (!f->has_L) throw Error(kErrContract, "the factor holds phase-1 tiles only (kPhase1 input)");
+    if (count < 0 || (count > 0 && (!ti || !tj || !payload))) throw Error(kErrInvalidArgument, "null tile arrays");
+    const int b = f->layout.b;
+    const size_t bb = static_cast<size_t>(b) * b;
+    // logdet: swap the replaced diagonal tiles' terms
+    double delta = 0.0;
+    std::vector<double> old(bb);
+    for (long k = 0; k < count; ++k) {
+      if (ti[k] != tj[k]) continue;
+      factor_tile_copy(*f, f->L, 1, ti + k, tj + k, old.data(), false);
+      for (int r = 0; r < b; ++r) {
+        const long row = static_cast<long>(ti[k]) * b + r;
+        if (row >= f->layout.n) break;
+        const double v = payload[static_cast<size_t>(k) * bb + static_cast<size_t>(r) * b + r];
+        if (!(v > 0.0)) throw Error(kErrConsistency, "factor diagonal entry " + std::to_string(row) + " is not positive");
+        delta += std::log(v) - std::log(old[static_cast<size_t>(r) * b + r]);
+      }
+    }
+    factor_tile_copy(*f, f->L, count, ti, tj, const_cast<double*>(payload), true);
+    f->logdet += 2.0 * delta;
+    run_phase1(*f);
   });
 }
 int tib_factor_logdet(tib_factor f, double* out) {
