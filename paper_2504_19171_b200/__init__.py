@@ -88,10 +88,10 @@ class Matrix:
     def __init__(self, handle: int):
         self._h = C.c_void_p(handle)
 
-    def __del__(self):
+    def __del__(self, _free=lib.tib_matrix_free):  # bound now: module globals are gone at interpreter exit
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            lib.tib_matrix_free(h)
+            _free(h)
             self._h = None
 
     def _info(self):
@@ -153,10 +153,10 @@ class Factor:
     def __init__(self, handle: int):
         self._h = C.c_void_p(handle)
 
-    def __del__(self):
+    def __del__(self, _free=lib.tib_factor_free):  # bound now: module globals are gone at interpreter exit
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            lib.tib_factor_free(h)
+            _free(h)
             self._h = None
 
     def _info(self):
@@ -244,10 +244,10 @@ class SelectedInverseResult:
     def __init__(self, handle: int):
         self._h = C.c_void_p(handle)
 
-    def __del__(self):
+    def __del__(self, _free=lib.tib_sigma_free):  # bound now: module globals are gone at interpreter exit
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            lib.tib_sigma_free(h)
+            _free(h)
             self._h = None
 
     def _info(self):
@@ -663,10 +663,10 @@ class Resident:
         return {"task_model_flops": m.value, "executed_flops": e.value, "logdet": ld.value,
                 "kernel_launches_per_rep": n.value}
 
-    def __del__(self):
+    def __del__(self, _free=lib.tib_resident_free):  # bound now: module globals are gone at interpreter exit
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            lib.tib_resident_free(h)
+            _free(h)
             self._h = None
 
 
