@@ -232,6 +232,10 @@ struct DevPlan {
   DevArray<DTask> chain;
   GraphCache graphs;
   std::mutex mu;
+  // reserved critical-queue workers when a launch carries more matrices than
+  // get dedicated chain SMs (-1: the plan's count).  Many chains keep q0 busy
+  // by themselves, and the bulk queue needs the workers more.
+  int crit_batch = -1;
 };
 
 struct FactorPlan2 {
@@ -257,6 +261,9 @@ static int crit_workers(bool factor) {
   const int all = env_int("TIB_CRIT_WORKERS", 0);
   if (all > 0) return all;
   return factor ? env_int("TIB_CRIT_WORKERS_FACTOR", 56) : env_int("TIB_CRIT_WORKERS_P2", 12);
+}
+static int crit_workers_batch(bool factor) {
+  return factor ? env_int("TIB_CRIT_BATCH_FACTOR", 8) : env_int("TIB_CRIT_BATCH_P2", 40);
 }
 
 static std::shared_ptr<DevPlan> upload_plan(DataflowPlan&& host, int device, cudaStream_t s) {
@@ -312,6 +319,7 @@ static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int 
                                                   env_int("TIB_FAT_LEAF", 0) != 0, env_int("TIB_CHAIN", 1) != 0,
                                                   env_int("TIB_CHAIN", 1) != 0 && env_int("TIB_BOUNDARY", 1) != 0),
                            device, s);
+  plan->flow->crit_batch = crit_workers_batch(true);
   plan->bp = plan->flow->host.bp;
   plan->nb = plan->flow->host.nb;
   std::lock_guard<std::mutex> lk(g_plan_mu);
@@ -331,6 +339,7 @@ static std::shared_ptr<Phase2Plan> phase2_plan_for(const Pattern& F, const Closu
   auto plan = std::make_shared<Phase2Plan>();
   plan->sel = sel;
   plan->flow = upload_plan(build_phase2_dataflow(F, plan->sel, crit_workers(false)), device, s);
+  plan->flow->crit_batch = crit_workers_batch(false);
   plan->bp = plan->flow->host.bp;
   plan->nb = plan->flow->host.nb;
   std::lock_guard<std::mutex> lk(g_plan_mu);
@@ -447,6 +456,7 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
                         : 0;
   // the chains' workers are reserved ones (worker 0 of the first CTAs): keep
   // the plan's count of reserved workers for the chain's helpers
+  if (!a.dedicate && P.crit_batch >= 0 && a.q0.workers > 0) a.q0.workers = P.crit_batch;
   if (a.static_chains) a.q0.workers += batch;
   a.poll_shift = env_int("TIB_POLL_SHIFT", 0);
   a.agent = a.dedicate && a.static_chains && env_int("TIB_AGENT", 1) ? 1 : 0;
@@ -850,7 +860,7 @@ static SigmaObj* selected_inverse_matrix(const MatrixObj& m, const Request& req,
     std::function<void()> up = [&]() {
       const auto h0 = std::chrono::steady_clock::now();
       CK(cudaStreamWaitEvent(rt.upload, cleared, 0));
-      for (int c = 0; c < m.layout.N; ++c) {
+      for (const int c : fp->flow->host.upload_order) {
         const size_t t0 = static_cast<size_t>(F.col_start(c)), t1 = static_cast<size_t>(F.col_start(c + 1));
         if (same)
           CK(cudaMemcpyAsync(st.A.p + t0 * bb, m.payload.p + t0 * bb, (t1 - t0) * bb * sizeof(double),
@@ -1649,9 +1659,17 @@ int tib_selected_inverse_batch(const tib_matrix* ms, int count, int device, doub
       if (!same) CK(cudaMemsetAsync(st.A.p, 0, T * tile * count * sizeof(double), s));
       std::function<void()> up = [&]() {
         CK(cudaStreamWaitEvent(rt.upload, cleared, 0));
-        for (int c = 0; c < N; c += grp)
+        // runs of consecutive columns in the plan's upload order, <= grp per copy
+        const std::vector<int>& ord = fp->flow->host.upload_order;
+        std::vector<std::pair<int, int>> runs;
+        for (size_t x = 0; x < ord.size();) {
+          size_t y = x + 1;
+          while (y < ord.size() && ord[y] == ord[y - 1] + 1 && static_cast<int>(y - x) < grp) ++y;
+          runs.push_back({ord[x], ord[y - 1] + 1});
+          x = y;
+        }
+        for (const auto& [c, ce] : runs)
           for (int k = 0; k < count; ++k) {
-            const int ce = std::min(N, c + grp);
             double* dA = st.A.p + T * tile * k;
             const size_t t0 = static_cast<size_t>(F.col_start(c)), t1 = static_cast<size_t>(F.col_start(ce));
             if (same)

@@ -728,20 +728,41 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
   // streamed upload: each task polls the upload counter of the latest tile
   // column of A it reads or writes
   {
+    // upload order: column c by the first column k whose elimination reads or
+    // updates one of its tiles (i, c) -- min k < c with (i, k) and (c, k) in F
+    // (the diagonal tile: any k with (c, k) in F), else c
+    std::vector<int> first(static_cast<size_t>(N));
+    {
+      std::vector<int> row_min(static_cast<size_t>(N), N);  // smallest column of each tile row
+      for (const Coord& c : F.tiles()) row_min[static_cast<size_t>(c.i)] = std::min(row_min[static_cast<size_t>(c.i)], c.j);
+      for (int c = 0; c < N; ++c) {
+        int k = std::min(c, row_min[static_cast<size_t>(c)]);
+        for (const int* r = F.rows_begin(c); r != F.rows_end(c); ++r) k = std::min(k, std::max(row_min[static_cast<size_t>(*r)], row_min[static_cast<size_t>(c)]));
+        first[static_cast<size_t>(c)] = k;
+      }
+    }
+    P.upload_order.resize(static_cast<size_t>(N));
+    for (int c = 0; c < N; ++c) P.upload_order[static_cast<size_t>(c)] = c;
+    std::stable_sort(P.upload_order.begin(), P.upload_order.end(),
+                     [&](int x, int y) { return first[static_cast<size_t>(x)] < first[static_cast<size_t>(y)]; });
+    std::vector<int> rank(static_cast<size_t>(N));
+    for (int r = 0; r < N; ++r) rank[static_cast<size_t>(P.upload_order[static_cast<size_t>(r)])] = r;
+    auto later = [&](int a, int b) { return a < 0 ? b : (b < 0 ? a : (rank[static_cast<size_t>(b)] > rank[static_cast<size_t>(a)] ? b : a)); };
     const long long tsz2 = static_cast<long long>(bp) * bp;
     auto col_of = [&](long long off) { return F.tiles()[static_cast<size_t>(off / tsz2)].j; };
     for (DTask& t : B.all) {
       int c = -1;
       if (t.kind == kLeafTask) {
         c = col_of(t.c_off);
-        if (t.mode & 4) c = std::max(c, col_of(P.segs[static_cast<size_t>(t.seg_begin)].b_off));
+        if (t.mode & 4) c = later(c, col_of(P.segs[static_cast<size_t>(t.seg_begin)].b_off));
+        if (t.mode & 4) c = later(c, col_of(t.p_off));
       } else {
-        if (t.c_store == kStoreA) c = std::max(c, col_of(t.c_off));
-        if (t.c0_store == kStoreA) c = std::max(c, col_of(t.c0_off));
+        if (t.c_store == kStoreA) c = later(c, col_of(t.c_off));
+        if (t.c0_store == kStoreA) c = later(c, col_of(t.c0_off));
         for (int k = t.seg_begin; k < t.seg_begin + t.seg_count; ++k) {
           const Seg& g = P.segs[static_cast<size_t>(k)];
-          if (g.a_store == kStoreA) c = std::max(c, col_of(g.a_off));
-          if (g.b_store == kStoreA) c = std::max(c, col_of(g.b_off));
+          if (g.a_store == kStoreA) c = later(c, col_of(g.a_off));
+          if (g.b_store == kStoreA) c = later(c, col_of(g.b_off));
         }
       }
       t.poll = c >= 0 ? static_cast<int>(cUpl + c) : -1;

@@ -43,6 +43,11 @@ struct DataflowPlan {
   // stream once tile column c of A is resident; every task and chain step that
   // touches the A store polls the counter of the latest column it touches
   long upl = -1;
+  // order in which the copy stream uploads the tile columns: by the first
+  // column whose elimination touches them (the arrow tip, updated by every
+  // column, goes up with the first columns instead of last); each task polls
+  // the counter of the touched column uploaded last
+  std::vector<int> upload_order;
 };
 
 // Fused factorization + phase 1 over the FILLED pattern: per column, the
