@@ -17,11 +17,12 @@
 // Two kernels, HBM-write bound then HBM-read bound:
 //   fill    one CTA per tile, one warp per row: every strictly lower entry,
 //           zeros elsewhere, identity on the padding (the diagonal comes next)
-//   rowsum  one thread per row x: the diagonal is 1 + the row's absolute
+//   rowsum  one thread per band row x: the diagonal is 1 + the row's absolute
 //           off-diagonal sum accumulated in the reference's draw order (own
 //           row ascending in c, then column x ascending in r), read back from
 //           the tiles just written -- the same sequential sum as the
-//           reference, so it matches to the last bit.
+//           reference, so it matches to the last bit; one warp per arrow row
+//           (arrow_rowsum_kernel), whose own row spans the whole matrix.
 // The target is a tile store in pattern slot order with row stride bp >= b
 // (the engine's A store; the slots may include fill-in tiles, which stay 0).
 #include <cuda_runtime.h>
@@ -150,10 +151,11 @@ __device__ __forceinline__ double seq_abs_sum(double s, const double* __restrict
   return s;
 }
 
-// After fill: diagonal entry x = 1 + sum |v| in draw order, from the stored tiles.
+// After fill: diagonal entry x = 1 + sum |v| in draw order, from the stored
+// tiles -- band rows (x < n - t), one thread each.
 __global__ void rowsum_kernel(Gen g, double* __restrict__ out) {
   const long long x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (x >= g.n) return;
+  if (x >= g.n - g.t) return;
   const long long ab = g.n - g.t;
   const long long bpp = static_cast<long long>(g.bp) * g.bp;
   const int X = static_cast<int>(x / g.b), xo = static_cast<int>(x % g.b);
@@ -183,6 +185,60 @@ __global__ void rowsum_kernel(Gen g, double* __restrict__ out) {
   out[slot_of(g, X, X) * bpp + static_cast<long long>(xo) * g.bp + xo] = s + 1.0;
 }
 
+// Arrow rows (x >= n - t), one warp each: the own row has x terms (up to n),
+// a serial chain that one thread would run at the load latency.  The warp
+// loads 256 consecutive terms (8 per lane) one chunk ahead, and every lane adds
+// the chunk in order from the shuffled values -- the same sequence of
+// additions (an added +0.0 past a chunk's end leaves s >= 0 unchanged), so the
+// same bits, at the FP64 add latency.
+__global__ void arrow_rowsum_kernel(Gen g, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const long long x = g.n - g.t + (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
+  if (x >= g.n) return;
+  const long long bpp = static_cast<long long>(g.bp) * g.bp;
+  const int X = static_cast<int>(x / g.b), xo = static_cast<int>(x % g.b);
+  // chunk c .. c + len (len <= 256, within one tile)
+  auto chunk_end = [&](long long c) {
+    const long long te = (c / g.b + 1) * g.b;
+    const long long e = c + 256 < te ? c + 256 : te;
+    return e < x ? e : x;
+  };
+  auto load = [&](long long c, long long e, double (&v)[8]) {
+    const int Jc = static_cast<int>(c / g.b);
+    const double* row = out + slot_of(g, X, Jc) * bpp + static_cast<long long>(xo) * g.bp + (c - static_cast<long long>(Jc) * g.b);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const long long i = lane * 8 + q;
+      v[q] = c + i < e ? __ldg(row + i) : 0.0;
+    }
+  };
+  double s = 0.0, cur[8], nxt[8];
+  long long c = 0, e = chunk_end(0);
+  if (c < x) load(c, e, cur);
+  while (c < x) {
+    const long long c2 = e, e2 = c2 < x ? chunk_end(c2) : c2;
+    if (c2 < x) load(c2, e2, nxt);
+#pragma unroll
+    for (int l = 0; l < 32; ++l)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s += fabs(__shfl_sync(0xffffffffu, cur[q], l));
+#pragma unroll
+    for (int q = 0; q < 8; ++q) cur[q] = nxt[q];
+    c = c2;
+    e = e2;
+  }
+  if (lane != 0) return;
+  // column x: the arrow rows below, r ascending
+  for (long long r = x + 1; r < g.n;) {
+    const int Ir = static_cast<int>(r / g.b);
+    const long long re = (static_cast<long long>(Ir) + 1) * g.b < g.n ? (static_cast<long long>(Ir) + 1) * g.b : g.n;
+    const double* col = out + slot_of(g, Ir, X) * bpp + xo + (r - static_cast<long long>(Ir) * g.b) * g.bp;
+    s = seq_abs_sum(s, col, re - r, g.bp);
+    r = re;
+  }
+  out[slot_of(g, X, X) * bpp + static_cast<long long>(xo) * g.bp + xo] = s + 1.0;
+}
+
 }  // namespace
 
 // colptr (N + 1) and rows (slots) describe the target pattern in device memory.
@@ -191,7 +247,8 @@ int launch_generate_arrowhead(long n, long w, long t, unsigned long long seed, i
   const Gen g{n, w, t, seed, b, bp, N, colptr, rows};
   if (N > 0 && max_col_slots > 0)
     fill_kernel<<<dim3(static_cast<unsigned>(max_col_slots), static_cast<unsigned>(N)), 256, 0, s>>>(g, out);
-  rowsum_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(g, out);
+  if (n - t > 0) rowsum_kernel<<<static_cast<unsigned>((n - t + 255) / 256), 256, 0, s>>>(g, out);
+  if (t > 0) arrow_rowsum_kernel<<<static_cast<unsigned>((t + 3) / 4), 128, 0, s>>>(g, out);
   return static_cast<int>(cudaGetLastError());
 }
 
