@@ -236,6 +236,7 @@ struct DevPlan {
   // get dedicated chain SMs (-1: the plan's count).  Many chains keep q0 busy
   // by themselves, and the bulk queue needs the workers more.
   int crit_batch = -1;
+  int c0_prefetch = 1;  // FlowArgs::c0_prefetch
 };
 
 struct FactorPlan2 {
@@ -320,6 +321,7 @@ static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int 
                                                   env_int("TIB_CHAIN", 1) != 0 && env_int("TIB_BOUNDARY", 1) != 0),
                            device, s);
   plan->flow->crit_batch = crit_workers_batch(true);
+  plan->flow->c0_prefetch = env_int("TIB_C0_PF_FACTOR", 1);
   plan->bp = plan->flow->host.bp;
   plan->nb = plan->flow->host.nb;
   std::lock_guard<std::mutex> lk(g_plan_mu);
@@ -340,6 +342,7 @@ static std::shared_ptr<Phase2Plan> phase2_plan_for(const Pattern& F, const Closu
   plan->sel = sel;
   plan->flow = upload_plan(build_phase2_dataflow(F, plan->sel, crit_workers(false)), device, s);
   plan->flow->crit_batch = crit_workers_batch(false);
+  plan->flow->c0_prefetch = env_int("TIB_C0_PF_P2", 1);
   plan->bp = plan->flow->host.bp;
   plan->nb = plan->flow->host.nb;
   std::lock_guard<std::mutex> lk(g_plan_mu);
@@ -461,6 +464,7 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
   a.poll_shift = env_int("TIB_POLL_SHIFT", 0);
   a.agent = a.dedicate && a.static_chains && env_int("TIB_AGENT", 1) ? 1 : 0;
   a.poll_uploads = poll ? 1 : 0;
+  a.c0_prefetch = P.c0_prefetch;
   a.watchdog_ns = static_cast<unsigned long long>(env_int("TIB_WATCHDOG_S", 60)) * 1000000000ull;
   a.slots0 = a.missing + nt * batch;
   a.slots1 = a.slots0 + static_cast<size_t>(P.host.q0.count) * batch;

@@ -21,6 +21,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 
 #include "taskfmt.hpp"
 
@@ -154,8 +155,18 @@ struct LocalSegs {
 // 16 DMMAs issue.  A segment's sign is applied by negating the accumulators
 // when the sign changes between chunks (at most a couple of times per task)
 // instead of per fragment.
+// C0 prefetch: a task whose initial value is final when it starts (no
+// second-phase dependency) stages C0 into the two ring stages the last chunks
+// free -- rows 0-31 and 32-63, row stride kLdC0 (conflict-free double2 reads)
+// -- so the epilogue's read of C0 is a shared-memory read, not an exposed
+// global round trip.  gemm_mainloop returns the ring stage of rows 0-31 (rows
+// 32-63 are in the next stage, mod kStages), or -1 when nothing was staged.
+constexpr int kLdC0 = kBN + 4;
+static_assert(32 * kLdC0 <= 2 * kStageDoubles, "a ring stage holds half a C0 block");
+
 template <class Src>
-__device__ __forceinline__ void gemm_mainloop(const RTask& t, const Src& src, double* smem, double (&acc)[4][4][2]) {
+__device__ __forceinline__ int gemm_mainloop(const RTask& t, const Src& src, double* smem, double (&acc)[4][4][2],
+                                             bool prefetch_c0 = false) {
   const int tid = wtid();
   const int lane = tid & 31, warp = tid >> 5;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
@@ -172,6 +183,7 @@ __device__ __forceinline__ void gemm_mainloop(const RTask& t, const Src& src, do
     const RSeg g = src.get(s);
     nchunks += (g.k_hi - g.k_lo) / kBK;
   }
+  prefetch_c0 = prefetch_c0 && t.C0 != nullptr && nchunks >= 4;
   int ls = 0, lk = 0;
   RSeg cur;
   cur.k_hi = 0;
@@ -205,7 +217,9 @@ __device__ __forceinline__ void gemm_mainloop(const RTask& t, const Src& src, do
   }
 
   bool negated = false;
-  for (int it = 0; it < nchunks; ++it) {
+  // one K chunk; the C0 prefetch is only compiled into the last iterations'
+  // copy (the main loop stays as it is without it)
+  auto chunk = [&](int it, auto with_c0) {
     cp_async_wait<kStages - 2>();
     wsync();
     {
@@ -217,6 +231,17 @@ __device__ __forceinline__ void gemm_mainloop(const RTask& t, const Src& src, do
         stage_flags = (stage_flags & ~(7u << (3 * st))) | (static_cast<uint32_t>(cur.flags & 7) << (3 * st));
         lk += kBK;
         settle();
+      }
+      if (decltype(with_c0)::value && it < nchunks - 1) {
+        // the stage of chunk it - 1: consumed (barrier above) and never refilled
+        double* dst = smem + ((it + kStages - 1) % kStages) * 2 * kStageDoubles;
+        const double* src0 = t.C0 + static_cast<size_t>(it - (nchunks - 3)) * 32 * t.ldc0;
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+          const int idx = tid + p * kGemmThreads;
+          const int r = idx >> 5, cq = (idx & 31) * 2;
+          cp_async16(dst + r * kLdC0 + cq, src0 + static_cast<size_t>(r) * t.ldc0 + cq);
+        }
       }
       cp_async_commit();
     }
@@ -259,7 +284,11 @@ __device__ __forceinline__ void gemm_mainloop(const RTask& t, const Src& src, do
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[cb][i], b[cb][j]);
     }
-  }
+  };
+  const int pf_from = prefetch_c0 ? nchunks - 3 : nchunks;  // C0 halves at chunks nchunks-3, nchunks-2
+  int it = 0;
+  for (; it < pf_from; ++it) chunk(it, std::false_type{});
+  for (; it < nchunks; ++it) chunk(it, std::true_type{});
   cp_async_wait<0>();
   if (negated) {
 #pragma unroll
@@ -270,7 +299,8 @@ __device__ __forceinline__ void gemm_mainloop(const RTask& t, const Src& src, do
         acc[i][j][1] = -acc[i][j][1];
       }
   }
-  wsync();  // every warp is done with the ring before the next task refills it
+  wsync();  // every warp is done with the ring before the next task refills it (and sees the staged C0)
+  return prefetch_c0 ? (nchunks + kStages - 4) % kStages : -1;
 }
 
 // Position of fragment (i, j, h) of the calling thread in the 64 x 64 block.
@@ -285,14 +315,22 @@ __device__ __forceinline__ int frag_col(int j) {
 
 // Epilogue: C = C0 + acc, written per mode; ends with a barrier so thread 0
 // may release the task's signals.
-__device__ __forceinline__ void gemm_epilogue(const RTask& t, const double (&acc)[4][4][2]) {
+// C0 comes from the ring stages gemm_mainloop staged it in (c0_stage >= 0,
+// smem = the ring) or from global memory.
+__device__ __forceinline__ void gemm_epilogue(const RTask& t, const double (&acc)[4][4][2], const double* smem = nullptr,
+                                              int c0_stage = -1) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int r = frag_row(i), c = frag_col(j);
       double v0 = acc[i][j][0], v1 = acc[i][j][1];
-      if (t.C0) {
+      if (c0_stage >= 0) {
+        const double* sc = smem + ((c0_stage + (r >> 5)) % kStages) * 2 * kStageDoubles + (r & 31) * kLdC0 + c;
+        const double2 o = *reinterpret_cast<const double2*>(sc);
+        v0 += o.x;
+        v1 += o.y;
+      } else if (t.C0) {
         const double2 o = __ldcg(reinterpret_cast<const double2*>(t.C0 + static_cast<size_t>(r) * t.ldc0 + c));
         v0 += o.x;
         v1 += o.y;
@@ -350,8 +388,8 @@ __device__ __forceinline__ void split_reduce(const double* slots, int parts, dou
 template <class Src>
 __device__ __forceinline__ void gemm_task(const RTask& t, const Src& src, double* smem) {
   double acc[4][4][2];
-  gemm_mainloop(t, src, smem, acc);
-  gemm_epilogue(t, acc);
+  const int c0s = gemm_mainloop(t, src, smem, acc, true);
+  gemm_epilogue(t, acc, smem, c0s);
 }
 
 __device__ __forceinline__ RTask resolve_task(const Task& s, const BaseTable& bt) {

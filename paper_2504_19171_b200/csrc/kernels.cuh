@@ -39,6 +39,7 @@ struct FlowArgs {
   int poll_shift;      // polling backoff caps scaled by 2^poll_shift
   int agent;           // with dedicate + static_chains: the chain's sibling worker raises its signals
   int poll_uploads;    // streamed upload: tasks wait for their A-store column (DTask::poll)
+  int c0_prefetch;     // plain tasks stage C0 in shared memory during their main loop
   unsigned long long watchdog_ns;  // a spin longer than this aborts the sweep (TIB_ERR_CUDA)
   unsigned long long* trace;
 };
