@@ -158,6 +158,26 @@ def test_streamed_upload_is_bitwise_identical(tib, monkeypatch):
     assert streamed.logdet() == upfront.logdet()
 
 
+def test_diagonal_tiles_lower_triangle_only(tib, monkeypatch):
+    """Diagonal tiles of A are significant in their lower triangle only (the
+    reference's potrf reads the lower part, kernels.cpp:48-69): garbage in the
+    strict upper part changes nothing, streamed upload or not."""
+    m = tib.generate(6000, 700, 60, 1.0, seed=29, tile_size=128)
+    ti, tj, pay = m.tiles()
+    ref = tib.selected_inverse(m, "pattern")
+    junk = pay.copy()
+    rng = np.random.default_rng(5)
+    up = np.triu(np.ones((128, 128), bool), 1)
+    for k in np.nonzero(ti == tj)[0]:
+        junk[k][up] = rng.uniform(-1e3, 1e3, up.sum())
+    mj = tib.from_tiles(m.n, 128, ti, tj, junk)
+    for stream in ("1", "0"):
+        monkeypatch.setenv("TIB_STREAM_UPLOAD", stream)
+        got = tib.selected_inverse(mj, "pattern")
+        assert got.checksum == ref.checksum, stream
+        assert got.logdet() == ref.logdet()
+
+
 def test_gapped_patterns_vs_dense(tib):
     """Tile patterns whose first off-diagonal tile is not j + 1: the chain's
     boundary step must write the next diagonal block back."""
