@@ -201,7 +201,17 @@ int tib_selected_inverse_batch(const tib_matrix* ms, int count, int device, doub
  * NULL buffers to query.  Layouts are the POD structs of taskfmt.hpp.        */
 typedef struct tib_resident_s* tib_resident;
 int tib_plan_export(tib_matrix m, int preset, const long* rows, const long* cols, long nentries, int which,
-                    int crit_workers, double* sizes, void* tasks, void* segs, void* deps, void* sigs);
+                    int crit_workers, int split, double* sizes, void* tasks, void* segs, void* deps, void* sigs);
+/* Two-chain elimination order of a single-matrix call: for a
+ * band + arrow tile pattern, order[k] (N entries, may be NULL) = the original
+ * tile at position k of [I_0 ascending, I_1 descending, separator, arrow];
+ * *split = first position of the second chain, -1 when the pattern admits no
+ * such order without fill.  No reference counterpart (the reference
+ * eliminates in natural order; results agree to rounding).                  */
+int tib_matrix_two_chain_order(tib_matrix m, int* order, int* split);
+/* The matrix symmetrically permuted into its two-chain order (host tiles;
+ * upper tiles of the original become transposed lower tiles).              */
+int tib_matrix_two_chain_permuted(tib_matrix m, tib_matrix* out);
 
 /* ---- timing support (bench.py) -------------------------------------------- */
 /* A device-resident copy of m with all sweep stores allocated; each run

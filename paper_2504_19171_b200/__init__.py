@@ -615,13 +615,31 @@ SEG_DTYPE = np.dtype({
 DEP_DTYPE = np.dtype([("counter", "<i4"), ("value", "<i4")])
 
 
-def plan_export(matrix: Matrix, selection="pattern", which: int = 0, crit_workers: int = 16) -> dict:
+def two_chain_order(matrix: Matrix):
+    """(order, split) of the matrix's two-chain elimination order (order[k] =
+    original tile at position k; split = first position of the second chain),
+    or (None, -1) when its tile pattern admits none without fill."""
+    split = C.c_int()
+    order = np.zeros(matrix.n_tiles, np.int32)
+    _check(lib.tib_matrix_two_chain_order(matrix._h, order.ctypes.data_as(C.POINTER(C.c_int)), C.byref(split)))
+    return (order, split.value) if split.value > 0 else (None, -1)
+
+
+def two_chain_permuted(matrix: Matrix) -> Matrix:
+    """The matrix symmetrically permuted into its two-chain order (host tiles)."""
+    h = _new_handle()
+    _check(lib.tib_matrix_two_chain_permuted(matrix._h, C.byref(h)))
+    return Matrix(h.value)
+
+
+def plan_export(matrix: Matrix, selection="pattern", which: int = 0, crit_workers: int = 16, split: int = -1) -> dict:
     """Host-built dataflow plan of one device sweep (0: factorization + phase 1,
-    1: phase 2 for `selection`) as numpy arrays; no GPU needed."""
+    1: phase 2 for `selection`) as numpy arrays; no GPU needed.  split > 0: the
+    factor plan with a second elimination chain from that column on."""
     preset, rows, cols, ne = _request(selection)
     sizes = np.zeros(10, np.float64)
     dptr = sizes.ctypes.data_as(C.POINTER(C.c_double))
-    _check(lib.tib_plan_export(matrix._h, preset, _lp(rows), _lp(cols), ne, which, crit_workers, dptr,
+    _check(lib.tib_plan_export(matrix._h, preset, _lp(rows), _lp(cols), ne, which, crit_workers, split, dptr,
                                None, None, None, None))
     nt, nq0, ns, nd, nsig, ncnt, bp, scratch, flops, tsz = sizes.tolist()
     if int(tsz) != DTASK_DTYPE.itemsize:
@@ -630,7 +648,7 @@ def plan_export(matrix: Matrix, selection="pattern", which: int = 0, crit_worker
     segs = np.zeros(int(ns), SEG_DTYPE)
     deps = np.zeros(int(nd), DEP_DTYPE)
     sigs = np.zeros(int(nsig), np.int32)
-    _check(lib.tib_plan_export(matrix._h, preset, _lp(rows), _lp(cols), ne, which, crit_workers, dptr,
+    _check(lib.tib_plan_export(matrix._h, preset, _lp(rows), _lp(cols), ne, which, crit_workers, split, dptr,
                                tasks.ctypes.data_as(C.c_void_p), segs.ctypes.data_as(C.c_void_p),
                                deps.ctypes.data_as(C.c_void_p), sigs.ctypes.data_as(C.c_void_p)))
     return {"tasks": tasks, "segs": segs, "deps": deps, "sigs": sigs, "q0": int(nq0), "counters": int(ncnt),
@@ -670,4 +688,4 @@ class Resident:
             self._h = None
 
 
-__all__ += ["plan_export", "Resident", "DTASK_DTYPE", "SEG_DTYPE", "DEP_DTYPE"]
+__all__ += ["plan_export", "two_chain_order", "two_chain_permuted", "Resident", "DTASK_DTYPE", "SEG_DTYPE", "DEP_DTYPE"]

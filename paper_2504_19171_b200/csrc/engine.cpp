@@ -161,6 +161,7 @@ struct DeviceRt {
   int dev = -1;
   cudaStream_t stream = nullptr;
   cudaStream_t upload = nullptr;  // streamed H2D of the A store, concurrent with the factor sweep
+  cudaStream_t permute = nullptr; // two-chain order: transposes of streamed tiles on the SMs the sweep leaves free
   int* one = nullptr;             // pinned host 1s (kOnes): the copy engine writes them into upload counters
   bool ready = false;
 };
@@ -185,6 +186,7 @@ static DeviceRt& runtime(int device) {
     CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
     CK(cudaStreamCreateWithFlags(&rt.stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&rt.upload, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&rt.permute, cudaStreamNonBlocking));
     CK(cudaMallocHost(reinterpret_cast<void**>(&rt.one), kOnes * sizeof(int)));
     for (int i = 0; i < kOnes; ++i) rt.one[i] = 1;
     CK(static_cast<cudaError_t>(configure_kernels()));
@@ -204,8 +206,8 @@ struct GraphCache {
     int* sched = nullptr;         // scheduler state: ctl[128], missing[batch x T], slots0, slots1
   };
   std::map<int, Entry> by_batch;
-  Entry& get(int batch, size_t ntasks, bool poll = false) {
-    Entry& e = by_batch[batch * 2 + (poll ? 1 : 0)];
+  Entry& get(int batch, size_t ntasks, bool poll = false, int grid = 0) {
+    Entry& e = by_batch[(grid * 65536 + batch) * 2 + (poll ? 1 : 0)];
     if (!e.tables) CK(cudaMalloc(reinterpret_cast<void**>(&e.tables), sizeof(BaseTable) * batch));
     if (!e.sched) CK(cudaMalloc(reinterpret_cast<void**>(&e.sched), (128 + 256 + 2 * ntasks * batch) * sizeof(int)));
     return e;
@@ -306,8 +308,9 @@ static std::mutex g_plan_mu;
 static std::map<std::pair<int, uint64_t>, std::shared_ptr<FactorPlan2>> g_fplans;
 static std::map<std::pair<int, uint64_t>, std::shared_ptr<Phase2Plan>> g_p2plans;
 
-static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int device, cudaStream_t s) {
-  const uint64_t key = pattern_hash(pattern, 1);
+static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int device, cudaStream_t s,
+                                                    int split = -1) {
+  const uint64_t key = pattern_hash(pattern, 1 + 0x9e3779b97f4a7c15ull * static_cast<uint64_t>(split + 2));
   {
     std::lock_guard<std::mutex> lk(g_plan_mu);
     auto it = g_fplans.find({device, key});
@@ -316,9 +319,12 @@ static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int 
   auto plan = std::make_shared<FactorPlan2>();
   plan->sym = symbolic_cholesky(pattern);
   plan->L = plan->sym.filled.layout();
-  plan->flow = upload_plan(build_factor_dataflow(plan->sym.filled, crit_workers(true), env_int("TIB_DEFER_W", 2),
+  // two chains keep the critical queue busier per reserved worker (tools/ab_env.py: 24 / 24 best)
+  const int crit = split > 0 ? env_int("TIB_CRIT_SPLIT_FACTOR", 24) : crit_workers(true);
+  plan->flow = upload_plan(build_factor_dataflow(plan->sym.filled, crit, env_int("TIB_DEFER_W", 2),
                                                   env_int("TIB_FAT_LEAF", 0) != 0, env_int("TIB_CHAIN", 1) != 0,
-                                                  env_int("TIB_CHAIN", 1) != 0 && env_int("TIB_BOUNDARY", 1) != 0),
+                                                  env_int("TIB_CHAIN", 1) != 0 && env_int("TIB_BOUNDARY", 1) != 0,
+                                                  split),
                            device, s);
   plan->flow->crit_batch = crit_workers_batch(true);
   plan->flow->c0_prefetch = env_int("TIB_C0_PF_FACTOR", 1);
@@ -331,8 +337,9 @@ static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int 
 }
 
 static std::shared_ptr<Phase2Plan> phase2_plan_for(const Pattern& F, const Closure& sel, int device,
-                                                   cudaStream_t s) {
-  const uint64_t key = pattern_hash(sel.closure, pattern_hash(F, 2));
+                                                   cudaStream_t s, int crit = -1) {
+  if (crit < 0) crit = crit_workers(false);
+  const uint64_t key = pattern_hash(sel.closure, pattern_hash(F, 2 + 7919ull * static_cast<uint64_t>(crit)));
   {
     std::lock_guard<std::mutex> lk(g_plan_mu);
     auto it = g_p2plans.find({device, key});
@@ -340,7 +347,7 @@ static std::shared_ptr<Phase2Plan> phase2_plan_for(const Pattern& F, const Closu
   }
   auto plan = std::make_shared<Phase2Plan>();
   plan->sel = sel;
-  plan->flow = upload_plan(build_phase2_dataflow(F, plan->sel, crit_workers(false)), device, s);
+  plan->flow = upload_plan(build_phase2_dataflow(F, plan->sel, crit), device, s);
   plan->flow->crit_batch = crit_workers_batch(false);
   plan->flow->c0_prefetch = env_int("TIB_C0_PF_P2", 1);
   plan->bp = plan->flow->host.bp;
@@ -419,13 +426,38 @@ static void write_trace(DevPlan& P, int batch, unsigned long long* d_trace, cuda
 // size into a CUDA graph; its only baked-in pointers are plan-owned).
 // pre_launch (streamed upload): issued after the counters are cleared and
 // before the sweep kernel; tasks then poll their A-store column's counter.
+// Chain tasks of a plan: the leading queue-0 tasks of kind kChainTask, each
+// initially ready (they are the first items of init0).
+static int chains_of(const DevPlan& P) {
+  int c = 0;
+  while (c < static_cast<int>(P.host.tasks.size()) && c < static_cast<int>(P.host.init0.size()) &&
+         P.host.tasks[static_cast<size_t>(c)].kind == kChainTask && P.host.init0[static_cast<size_t>(c)] == c)
+    ++c;
+  return c;
+}
+
+// grid > 0: launch that many persistent CTAs instead of one per SM (the
+// two-chain streamed upload leaves SMs free for its transposes).
+// Streamed two-chain upload: the in-kernel transpose agents' work lists.
+struct TransposeAgents {
+  int agents = 0, ncols = 0, bp = 0;
+  const int* cols = nullptr;
+  const int* off = nullptr;
+  const int* dst = nullptr;
+  const int* src = nullptr;
+  const unsigned char* tr = nullptr;
+  long long raw = 0, upl = 0, arrive = 0;
+};
+
 static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStream_t s,
-                     const std::function<void()>* pre_launch = nullptr, cudaEvent_t cleared = nullptr) {
+                     const std::function<void()>* pre_launch = nullptr, cudaEvent_t cleared = nullptr, int grid = 0,
+                     const TransposeAgents* ta = nullptr) {
   std::lock_guard<std::mutex> lk(P.mu);
   const int batch = static_cast<int>(tables.size());
   const size_t nt = P.host.tasks.size();
   const bool poll = pre_launch != nullptr;
-  GraphCache::Entry& e = P.graphs.get(batch, nt, poll);
+  if (grid <= 0 || grid > P.grid) grid = P.grid;
+  GraphCache::Entry& e = P.graphs.get(batch, nt, poll, ta ? 1 : (grid == P.grid ? 0 : grid));
   CK(cudaMemcpyAsync(e.tables, tables.data(), sizeof(BaseTable) * batch, cudaMemcpyHostToDevice, s));
   for (const BaseTable& t : tables)
     CK(cudaMemsetAsync(t.p[kStoreCounters], 0, static_cast<size_t>(P.host.counters) * sizeof(int), s));
@@ -452,26 +484,37 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
   a.ctl = e.sched;
   a.missing = e.sched + 128 + 256;  // (ctl lines, 256 spare ints, then the per-task counts)
   a.chain = P.chain.p;
-  a.dedicate = batch <= env_int("TIB_DEDICATE_MAX_BATCH", 4) ? 1 : 0;
-  a.static_chains = (!P.host.chain.empty() && !P.host.init0.empty() && P.host.init0[0] == 0 &&
-                     P.host.tasks[0].kind == kChainTask && batch <= P.grid)
-                        ? 1
-                        : 0;
+  const int nchains = chains_of(P);
+  a.dedicate = batch * std::max(nchains, 1) <= env_int("TIB_DEDICATE_MAX_BATCH", 4) ? 1 : 0;
+  a.static_chains = nchains > 0 && batch * nchains <= grid ? nchains : 0;
   // the chains' workers are reserved ones (worker 0 of the first CTAs): keep
   // the plan's count of reserved workers for the chain's helpers
   if (!a.dedicate && P.crit_batch >= 0 && a.q0.workers > 0) a.q0.workers = P.crit_batch;
-  if (a.static_chains) a.q0.workers += batch;
+  a.q0.workers += batch * a.static_chains;
   a.poll_shift = env_int("TIB_POLL_SHIFT", 0);
   a.agent = a.dedicate && a.static_chains && env_int("TIB_AGENT", 1) ? 1 : 0;
   a.poll_uploads = poll ? 1 : 0;
   a.c0_prefetch = P.c0_prefetch;
   a.watchdog_ns = static_cast<unsigned long long>(env_int("TIB_WATCHDOG_S", 60)) * 1000000000ull;
+  if (ta && batch == 1) {
+    a.t_agents = ta->agents;
+    a.t_ncols = ta->ncols;
+    a.t_bp = ta->bp;
+    a.t_cols = ta->cols;
+    a.t_off = ta->off;
+    a.t_dst = ta->dst;
+    a.t_src = ta->src;
+    a.t_tr = ta->tr;
+    a.t_raw = ta->raw;
+    a.t_upl = ta->upl;
+    a.t_arrive = ta->arrive;
+  }
   a.slots0 = a.missing + nt * batch;
   a.slots1 = a.slots0 + static_cast<size_t>(P.host.q0.count) * batch;
   a.trace = nullptr;
   auto enqueue = [&]() {
     launch_zero_strips(P.zero.p, static_cast<int>(P.zero.n), P.host.bp, batch, e.tables, s);
-    launch_dataflow(a, P.need.p, P.init0.p, static_cast<int>(P.init0.n), P.init1.p, static_cast<int>(P.init1.n), P.grid, s);
+    launch_dataflow(a, P.need.p, P.init0.p, static_cast<int>(P.init0.n), P.init1.p, static_cast<int>(P.init1.n), grid, s);
   };
   if (std::getenv("TIB_CHAIN_PROF") && set_chain_profile(nullptr) == cudaSuccess) {
     // phases: 0 leaf (10 chol32 A00, 11 coupling DMMA, 12 chol32 A11, 13 X10 DMMA, rest: logdet + stores),
@@ -508,7 +551,7 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
     CK(cudaFreeAsync(d_trace, s));
     return;
   }
-  if (!use_graphs()) {
+  if (!use_graphs() || ta) {  // (the agents' work lists are per call: no cached graph)
     enqueue();
     CK(cudaGetLastError());
     launched();
@@ -534,15 +577,17 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
 // launches of the same plan.
 static size_t max_batch(const DevPlan& P) {
   const size_t by_items = static_cast<size_t>(INT_MAX) / std::max<size_t>(P.host.tasks.size(), 1);
-  const size_t by_chains = P.host.chain.empty() ? by_items : static_cast<size_t>(P.grid);
+  const size_t by_chains =
+      P.host.chain.empty() ? by_items : static_cast<size_t>(P.grid) / static_cast<size_t>(std::max(chains_of(P), 1));
   return std::max<size_t>(1, std::min(by_items, by_chains));
 }
 
 static void run_flow_chunked(DevPlan& P, const std::vector<BaseTable>& tables, cudaStream_t s,
-                             const std::function<void()>* pre_launch = nullptr, cudaEvent_t cleared = nullptr) {
+                             const std::function<void()>* pre_launch = nullptr, cudaEvent_t cleared = nullptr,
+                             int grid = 0, const TransposeAgents* ta = nullptr) {
   const size_t mb = max_batch(P);
   if (tables.size() <= mb) {
-    run_flow(P, tables, s, pre_launch, cleared);
+    run_flow(P, tables, s, pre_launch, cleared, grid, ta);
     return;
   }
   if (pre_launch) throw Error(kErrInvalidArgument, "streamed upload is single-launch only");
@@ -622,6 +667,35 @@ static const double* host_payload(const MatrixObj& m) {
     CK(cudaStreamSynchronize(rt.stream));
   }
   return m.payload.p;
+}
+
+// Host payload of m in the two-chain order, bp-layout tiles over so.permuted
+// (identity on the padded diagonal, zero fill-in): permuted tile (i, j) is
+// original tile (order[i], order[j]), or the transpose of (order[j], order[i]).
+static void permuted_payload(const MatrixObj& m, const SplitOrder& so, int bp, double* out) {
+  const int b = m.layout.b;
+  const double* src = host_payload(m);
+  const size_t bb = static_cast<size_t>(b) * b, bpp = static_cast<size_t>(bp) * bp;
+  const Pattern& P = so.permuted;
+  for (size_t k = 0; k < P.size(); ++k) {
+    const Coord& c = P.tiles()[k];
+    double* dst = out + k * bpp;
+    std::memset(dst, 0, bpp * sizeof(double));
+    bool tr = false;
+    const Coord o = split_source(so, c.i, c.j, tr);
+    const long sl = m.pattern.slot(o.i, o.j);
+    if (sl >= 0) {
+      const double* t = src + static_cast<size_t>(sl) * bb;
+      if (!tr) {
+        for (int r = 0; r < b; ++r) std::memcpy(dst + static_cast<size_t>(r) * bp, t + static_cast<size_t>(r) * b, b * sizeof(double));
+      } else {
+        for (int r = 0; r < b; ++r)
+          for (int q = 0; q < b; ++q) dst[static_cast<size_t>(r) * bp + q] = t[static_cast<size_t>(q) * b + r];
+      }
+    }
+    if (c.i == c.j)
+      for (int r = b; r < bp; ++r) dst[static_cast<size_t>(r) * bp + r] = 1.0;
+  }
 }
 
 // TiledFactor (storage.hpp:46-51), device resident.  has_L: the factor tiles L
@@ -784,9 +858,10 @@ static double reduce_logdet(const double* parts, int N, int nb) {
 
 // Runs the fused factor sweep for the matrices already resident in their A stores.
 static void factor_sweep(FactorPlan2& P, SweepStores& st, cudaStream_t s, const std::vector<BaseTable>& tables,
-                         const std::function<void()>* pre_launch = nullptr, cudaEvent_t cleared = nullptr) {
+                         const std::function<void()>* pre_launch = nullptr, cudaEvent_t cleared = nullptr,
+                         int grid = 0, const TransposeAgents* ta = nullptr) {
   CK(cudaMemsetAsync(st.status.p, 0xff, tables.size() * sizeof(unsigned long long), s));
-  run_flow_chunked(*P.flow, tables, s, pre_launch, cleared);
+  run_flow_chunked(*P.flow, tables, s, pre_launch, cleared, grid, ta);
 }
 
 static void phase2_sweep(Phase2Plan& P, cudaStream_t s, const std::vector<BaseTable>& tables) {
@@ -821,8 +896,287 @@ static Request make_request(int preset, const long* rows, const long* cols, long
   return r;
 }
 
+// ---------------------------------------------------------------------------
+// Two-chain order of a single-matrix call (planner.hpp two_chain_order): the
+// sweeps run on the symmetrically permuted matrix, whose factor has two
+// independent elimination chains; Sigma comes back in the natural order.
+struct SplitCall {
+  FactorPlan natural;  // the matrix's own filled pattern
+  Closure sel;         // the request's closure (== natural.filled)
+  SplitOrder so;
+  // per permuted slot: source slot in m.pattern (-1: fill-in), in the natural
+  // filled pattern, and whether the permuted tile is the source's transpose
+  std::vector<int> src, src_filled;
+  std::vector<unsigned char> tr;
+};
+
+static bool split_call(const MatrixObj& m, const Request& req, SplitCall& sc) {
+  if (env_int("TIB_SPLIT", 1) == 0) return false;
+  sc.natural = symbolic_cholesky(m.pattern);
+  const Pattern& F = sc.natural.filled;
+  // chain-bound sweeps only: the update work per chain step grows with the
+  // square of the tiles per column and of the blocks per tile
+  const double per_col = static_cast<double>(F.size() - static_cast<size_t>(F.layout().N)) / F.layout().N;
+  const double nbk = static_cast<double>((F.layout().b + 63) / 64);
+  if (per_col * per_col * nbk * nbk > env_int("TIB_SPLIT_WORK", 3000)) return false;
+  sc.sel = symbolic_inversion(select_tiles(F.layout(), F, req), F);
+  if (!(sc.sel.closure == F)) return false;  // Sigma on the whole factor pattern only
+  sc.so = two_chain_order(F);
+  if (sc.so.split <= 0) return false;
+  const Pattern& P = sc.so.permuted;
+  sc.src.resize(P.size());
+  sc.src_filled.resize(P.size());
+  sc.tr.resize(P.size());
+  for (size_t k = 0; k < P.size(); ++k) {
+    bool t = false;
+    const Coord o = split_source(sc.so, P.tiles()[k].i, P.tiles()[k].j, t);
+    sc.src[k] = static_cast<int>(m.pattern.slot(o.i, o.j));
+    sc.src_filled[k] = static_cast<int>(F.slot(o.i, o.j));
+    sc.tr[k] = t ? 1 : 0;
+  }
+  return true;
+}
+
+template <class T>
+static DevBuf to_device(const std::vector<T>& v, int dev, cudaStream_t s) {
+  DevBuf d((v.size() * sizeof(T) + 7) / 8 + 1, dev, s);
+  if (!v.empty()) CK(cudaMemcpyAsync(d.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));  // the host vector may die with the caller's scope
+  return d;
+}
+
+// Sigma' (permuted closure = permuted filled pattern) -> the natural closure
+// store; marginal variances likewise (tile rows).  Device maps built once.
+struct Unpermute {
+  DevBuf d, src, tr, rd, rs;
+  int count = 0, N = 0;
+  Unpermute(const SplitCall& sc, int dev, cudaStream_t s) {
+    const Pattern& C = sc.sel.closure;
+    const Pattern& P = sc.so.permuted;
+    std::vector<int> vd(C.size()), vs(C.size());
+    std::vector<unsigned char> vt(C.size());
+    for (size_t k = 0; k < C.size(); ++k) {
+      const Coord c = C.tiles()[k];
+      const int a = sc.so.pos[static_cast<size_t>(c.i)], b = sc.so.pos[static_cast<size_t>(c.j)];
+      vd[k] = static_cast<int>(k);
+      vs[k] = static_cast<int>(a >= b ? P.slot(a, b) : P.slot(b, a));
+      vt[k] = a < b ? 1 : 0;
+    }
+    N = C.layout().N;
+    std::vector<int> vrd(static_cast<size_t>(N)), vrs(static_cast<size_t>(N));
+    for (int i = 0; i < N; ++i) {
+      vrd[static_cast<size_t>(i)] = i;
+      vrs[static_cast<size_t>(i)] = sc.so.pos[static_cast<size_t>(i)];
+    }
+    count = static_cast<int>(C.size());
+    d = to_device(vd, dev, s);
+    src = to_device(vs, dev, s);
+    tr = to_device(vt, dev, s);
+    rd = to_device(vrd, dev, s);
+    rs = to_device(vrs, dev, s);
+  }
+  void run(const double* from, double* to, const double* var_from, double* var_to, int bp, cudaStream_t s) const {
+    launch_permute_tiles(to, from, reinterpret_cast<const int*>(d.p), reinterpret_cast<const int*>(src.p),
+                         reinterpret_cast<const unsigned char*>(tr.p), count, bp, 148 * 8, s);
+    launch_permute_rows(var_to, var_from, reinterpret_cast<const int*>(rd.p), reinterpret_cast<const int*>(rs.p), N,
+                        bp, s);
+    CK(cudaGetLastError());
+  }
+};
+
+static SigmaObj* selected_inverse_split(const MatrixObj& m, const Request& req, int device, SplitCall& sc) {
+  DeviceRt& rt = runtime(device);
+  cudaStream_t s = rt.stream;
+  HostTimer tm(s);
+  auto fp = factor_plan_for(sc.so.permuted, device, s, sc.so.split);
+  const Pattern& Fp = fp->sym.filled;
+  Request preq;
+  preq.preset = kFactorPattern;
+  const Closure selp = symbolic_inversion(select_tiles(Fp.layout(), Fp, preq), Fp);
+  auto p2 = phase2_plan_for(Fp, selp, device, s, env_int("TIB_CRIT_SPLIT_P2", 24));
+  tm.mark("plans");
+  const int bp = fp->bp, N = m.layout.N;
+  const size_t bb = static_cast<size_t>(bp) * bp, T = Fp.size();
+  SweepStores st;
+  // counters: the plans', then (streamed upload) a raw upload counter and an
+  // agents' arrival counter per column
+  const long fc = fp->flow->host.counters;
+  alloc_factor_stores(st, *fp, 1, device, s, std::max<long>(p2->flow->host.counters, fc + 2L * N),
+                      p2->flow->host.scratch_doubles);
+  auto* res = new SigmaObj;
+  std::unique_ptr<SigmaObj> guard(res);
+  res->device = device;
+  res->layout = m.layout;
+  res->req = req;
+  auto nat = std::make_shared<Phase2Plan>();  // the natural closure (accessors); no device plan
+  nat->sel = sc.sel;
+  nat->bp = bp;
+  nat->nb = p2->nb;
+  res->plan = nat;
+  res->S = DevBuf(sc.sel.closure.size() * bb, device, s);  // staging of transposed tiles, then Sigma
+  res->var = DevBuf(static_cast<size_t>(N) * bp, device, s);
+  DevBuf varp(static_cast<size_t>(N) * bp, device, s);
+  tm.mark("allocations");
+  // factor sweep on the permuted A store; phase 2 writes Sigma' over A (dead by then)
+  std::vector<BaseTable> tf{make_table(st.A.p, st.L.p, st.P1.p, res->S.p, varp.p, st.scratch.p, st.logdet.p,
+                                       st.status.p, st.ctr(0))};
+  std::vector<BaseTable> tp{make_table(st.A.p, st.L.p, st.P1.p, st.A.p, varp.p, st.scratch.p, st.logdet.p,
+                                       st.status.p, st.ctr(0))};
+  const bool stream_up = !m.gen.on && bp == m.layout.b && m.payload.pinned && env_int("TIB_STREAM_UPLOAD", 1) != 0 &&
+                         fp->flow->host.upl >= 0;
+  if (m.gen.on) {
+    // natural tiles from the device generator into the staging store, then permuted
+    device_generate(m, sc.natural.filled, bp, res->S.p, s);
+    std::vector<int> d(T);
+    for (size_t k = 0; k < T; ++k) d[k] = static_cast<int>(k);
+    DevBuf dd = to_device(d, device, s), ds = to_device(sc.src_filled, device, s), dt = to_device(sc.tr, device, s);
+    launch_permute_tiles(st.A.p, res->S.p, reinterpret_cast<const int*>(dd.p), reinterpret_cast<const int*>(ds.p),
+                         reinterpret_cast<const unsigned char*>(dt.p), static_cast<int>(T), bp, 148 * 8, s);
+    CK(cudaGetLastError());
+    tm.mark("generate");
+    factor_sweep(*fp, st, s, tf);
+  } else if (!stream_up) {
+    HostBuf hb(T * bb);
+    permuted_payload(m, sc.so, bp, hb.p);
+    CK(cudaMemcpyAsync(st.A.p, hb.p, T * bb * sizeof(double), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    tm.mark("upload");
+    factor_sweep(*fp, st, s, tf);
+  } else {
+    // Streamed, permuted column by column in the plan's upload order.  A
+    // natural tile column whose tiles all land, in order, in one permuted
+    // column (I_0, the arrow) goes up as one copy straight into A; every
+    // other natural column goes up as one copy into the staging store (the
+    // Sigma store, in the matrix's own slot layout), and the kernel's agents
+    // (worker 1 of the last TIB_SPLIT_AGENTS CTAs) copy or transpose its
+    // tiles into A.  The copy engine sets a raw counter per permuted column
+    // once every source column it needs is up; the agents release the
+    // column's upload counter in upload order (tasks poll one column: the
+    // touched one uploaded last).  (A second kernel beside the persistent
+    // sweep would share a hardware queue with it and wait behind it.)
+    int* ctr = reinterpret_cast<int*>(st.ctr(0));
+    const bool fill = !(sc.natural.filled == m.pattern);
+    if (fill) CK(cudaMemsetAsync(st.A.p, 0, T * bb * sizeof(double), s));
+    CK(cudaMemsetAsync(ctr + fc, 0, 2 * static_cast<size_t>(N) * sizeof(int), s));
+    const Pattern& Mp = m.pattern;
+    // direct natural columns: slot k of column j -> permuted slot base + (k - start)
+    std::vector<long> direct(static_cast<size_t>(N), -1);
+    for (int j = 0; j < N; ++j) {
+      const long k0 = Mp.col_start(j), k1 = Mp.col_start(j + 1);
+      const int pj = sc.so.pos[static_cast<size_t>(j)];
+      long base = -1;
+      bool ok = k1 > k0;
+      for (long k = k0; k < k1 && ok; ++k) {
+        const int pi = sc.so.pos[static_cast<size_t>(Mp.tiles()[static_cast<size_t>(k)].i)];
+        if (pi < pj) {
+          ok = false;
+          break;
+        }
+        const long d = Fp.slot(pi, pj);
+        if (k == k0) base = d;
+        ok = d == base + (k - k0);
+      }
+      if (ok) direct[static_cast<size_t>(j)] = base;
+    }
+    // agents' entries per permuted column, and each column's source columns
+    std::vector<int> edst, esrc, eoff(static_cast<size_t>(N) + 1, 0);
+    std::vector<unsigned char> etr;
+    std::vector<std::vector<int>> need(static_cast<size_t>(N));
+    for (int c = 0; c < N; ++c) {
+      for (long k = Fp.col_start(c); k < Fp.col_start(c + 1); ++k) {
+        const int sk = sc.src[static_cast<size_t>(k)];
+        if (sk < 0) continue;  // fill-in: zeroed above
+        const int nj = Mp.tiles()[static_cast<size_t>(sk)].j;
+        need[static_cast<size_t>(c)].push_back(nj);
+        if (direct[static_cast<size_t>(nj)] >= 0) continue;
+        edst.push_back(static_cast<int>(k));
+        esrc.push_back(sk);
+        etr.push_back(sc.tr[static_cast<size_t>(k)]);
+      }
+      eoff[static_cast<size_t>(c) + 1] = static_cast<int>(edst.size());
+    }
+    DevBuf dd = to_device(edst, device, s), dsrc = to_device(esrc, device, s), dtr = to_device(etr, device, s),
+           doff = to_device(eoff, device, s), dcols = to_device(fp->flow->host.upload_order, device, s);
+    TransposeAgents ta;
+    ta.agents = std::max(1, std::min(env_int("TIB_SPLIT_AGENTS", 8), fp->flow->grid - 4));
+    ta.ncols = N;
+    ta.bp = bp;
+    ta.cols = reinterpret_cast<const int*>(dcols.p);
+    ta.off = reinterpret_cast<const int*>(doff.p);
+    ta.dst = reinterpret_cast<const int*>(dd.p);
+    ta.src = reinterpret_cast<const int*>(dsrc.p);
+    ta.tr = reinterpret_cast<const unsigned char*>(dtr.p);
+    ta.raw = fc;
+    ta.arrive = fc + N;
+    ta.upl = fp->flow->host.upl;
+    cudaEvent_t cleared, uploaded;
+    CK(cudaEventCreateWithFlags(&cleared, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&uploaded, cudaEventDisableTiming));
+    std::vector<char> sent(static_cast<size_t>(N), 0);
+    std::function<void()> up = [&]() {
+      CK(cudaStreamWaitEvent(rt.upload, cleared, 0));
+      for (const int c : fp->flow->host.upload_order) {
+        for (const int nj : need[static_cast<size_t>(c)]) {
+          if (sent[static_cast<size_t>(nj)]) continue;
+          sent[static_cast<size_t>(nj)] = 1;
+          const long k0 = Mp.col_start(nj), k1 = Mp.col_start(nj + 1);
+          const long d = direct[static_cast<size_t>(nj)];
+          double* dst = d >= 0 ? st.A.p + static_cast<size_t>(d) * bb : res->S.p + static_cast<size_t>(k0) * bb;
+          CK(cudaMemcpyAsync(dst, m.payload.p + static_cast<size_t>(k0) * bb, static_cast<size_t>(k1 - k0) * bb * sizeof(double),
+                             cudaMemcpyHostToDevice, rt.upload));
+        }
+        CK(cudaMemcpyAsync(ctr + fc + c, rt.one, sizeof(int), cudaMemcpyHostToDevice, rt.upload));
+      }
+      CK(cudaEventRecord(uploaded, rt.upload));
+    };
+    factor_sweep(*fp, st, s, tf, &up, cleared, 0, &ta);
+    CK(cudaStreamWaitEvent(s, uploaded, 0));
+    CK(cudaStreamSynchronize(s));  // the events and device lists die with this scope
+    cudaEventDestroy(cleared);
+    cudaEventDestroy(uploaded);
+  }
+  tm.mark("factor sweep");
+  phase2_sweep(*p2, s, tp);
+  tm.mark("phase-2 sweep");
+  Unpermute(sc, device, s).run(st.A.p, res->S.p, varp.p, res->var.p, bp, s);
+  tm.mark("unpermute");
+  std::vector<double> parts(fp->flow->host.logdet_doubles);
+  CK(cudaMemcpyAsync(parts.data(), st.logdet.p, parts.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  check_status(st.status, 1, m.layout, s);  // a NotSpd here is re-run in the natural order by the caller
+  tm.mark("read-back");
+  res->logdet = reduce_logdet(parts.data(), N, fp->nb);
+  return guard.release();
+}
+
 // fused factorize + phase 2 for one matrix; returns the result object
-static SigmaObj* selected_inverse_matrix(const MatrixObj& m, const Request& req, int device) {
+static SigmaObj* selected_inverse_matrix(const MatrixObj& m, const Request& req, int device, bool allow_split = true) {
+  // The two-chain order pays off when the factor sweep is bound by its chain:
+  // always for A already on the device (the device generator), and for a host
+  // matrix streamed up under the sweep only if the natural chain (~30 us per
+  // 64-column step) is clearly longer than the upload (~50 GB/s); otherwise
+  // the sweep waits for the upload in either order, and the split order's
+  // chains, twice as fast as the upload, leave tasks polling for columns
+  // (large config: 216 vs 203 ms).  TIB_SPLIT_STREAMED=1/0 forces it.
+  const bool streams = !m.gen.on && m.payload.pinned && m.layout.b % 64 == 0 && env_int("TIB_STREAM_UPLOAD", 1) != 0;
+  bool split_ok = !streams;
+  if (streams) {
+    const int forced = env_int("TIB_SPLIT_STREAMED", -1);
+    const double chain_ms = m.layout.N * ((m.layout.b + 63) / 64) * 0.030;
+    const double upload_ms = static_cast<double>(m.pattern.size()) * m.layout.b * m.layout.b * 8 / 50e6;
+    split_ok = forced >= 0 ? forced != 0 : chain_ms > 1.3 * upload_ms;
+  }
+  if (allow_split && split_ok) {
+    SplitCall sc;
+    if (split_call(m, req, sc)) {
+      try {
+        return selected_inverse_split(m, req, device, sc);
+      } catch (const NotSpd&) {
+        // the failing pivot of the permuted elimination is not the reference's:
+        // the natural order reports the first non-positive pivot like factorize
+        return selected_inverse_matrix(m, req, device, false);
+      }
+    }
+  }
   DeviceRt& rt = runtime(device);
   cudaStream_t s = rt.stream;
   HostTimer tm(s);
@@ -1733,8 +2087,34 @@ int tib_selected_inverse_batch(const tib_matrix* ms, int count, int device, doub
   });
 }
 
+int tib_matrix_two_chain_order(tib_matrix m, int* order, int* split) {
+  return guarded([&] {
+    need(m, "matrix");
+    const SplitOrder so = two_chain_order(symbolic_cholesky(m->pattern).filled);
+    if (split) *split = so.split;
+    if (order && so.split > 0) std::copy(so.order.begin(), so.order.end(), order);
+  });
+}
+
+int tib_matrix_two_chain_permuted(tib_matrix m, tib_matrix* out) {
+  return guarded([&] {
+    need(m, "matrix");
+    if (!out) throw Error(kErrInvalidArgument, "null output handle");
+    const SplitOrder so = two_chain_order(symbolic_cholesky(m->pattern).filled);
+    if (so.split <= 0) throw Error(kErrInvalidArgument, "the tile pattern admits no two-chain order");
+    const int b = m->layout.b;
+    HostBuf hb(so.permuted.size() * static_cast<size_t>(b) * b);
+    permuted_payload(*m, so, b, hb.p);
+    auto* r = new tib_matrix_s;
+    r->layout = m->layout;
+    r->pattern = so.permuted;
+    r->payload = std::move(hb);
+    *out = r;
+  });
+}
+
 int tib_plan_export(tib_matrix m, int preset, const long* rows, const long* cols, long ne, int which,
-                    int crit_workers, double* sizes, void* tasks, void* segs, void* deps, void* sigs) {
+                    int crit_workers, int split, double* sizes, void* tasks, void* segs, void* deps, void* sigs) {
   return guarded([&] {
     need(m, "matrix");
     if (which != 0 && which != 1) throw Error(kErrInvalidArgument, "which must be 0 (factor) or 1 (phase 2)");
@@ -1745,7 +2125,7 @@ int tib_plan_export(tib_matrix m, int preset, const long* rows, const long* cols
       // the CPU simulator runs the same decomposition as the GPU chain, with the
       // chain's steps kept as (fat / boundary) leaf tasks
       P = build_factor_dataflow(sym.filled, crit_workers, env_int("TIB_DEFER_W", 2), env_int("TIB_FAT_LEAF", 0) != 0,
-                                false, env_int("TIB_CHAIN", 1) != 0 && env_int("TIB_BOUNDARY", 1) != 0);
+                                false, env_int("TIB_CHAIN", 1) != 0 && env_int("TIB_BOUNDARY", 1) != 0, split);
     } else {
       const Closure sel =
           symbolic_inversion(select_tiles(sym.filled.layout(), sym.filled, make_request(preset, rows, cols, ne)), sym.filled);
@@ -1783,6 +2163,11 @@ struct tib_resident_s {
   std::vector<BaseTable> tables;
   double logdet = 0;
   double model_flops = 0;
+  // two-chain order (one matrix): the stores hold the permuted matrix, and
+  // each run ends with Sigma / the variances un-permuted into Sn / varn
+  std::unique_ptr<SplitCall> split;
+  std::unique_ptr<Unpermute> unperm;
+  DevBuf Sn, varn;
 };
 
 extern "C" {
@@ -1804,22 +2189,46 @@ int tib_resident_create_batch(const tib_matrix* ms, int count, int device, tib_r
     r->device = device;
     r->count = count;
     r->layout = m->layout;
-    r->fp = factor_plan_for(m->pattern, device, s);
-    const Pattern& F = r->fp->sym.filled;
+    // a single matrix runs in the two-chain order (bit-for-bit the work of the
+    // public call, which uses it too)
+    const FactorPlan natural = symbolic_cholesky(m->pattern);
     Request req;
     req.preset = kFactorPattern;
+    {
+      auto sc = std::make_unique<SplitCall>();
+      if (count == 1 && split_call(*m, req, *sc)) r->split = std::move(sc);
+    }
+    const SplitOrder* so = r->split ? &r->split->so : nullptr;
+    r->fp = so ? factor_plan_for(so->permuted, device, s, so->split) : factor_plan_for(m->pattern, device, s);
+    const Pattern& F = r->fp->sym.filled;
     const Closure sel = symbolic_inversion(select_tiles(F.layout(), F, req), F);
-    r->p2 = phase2_plan_for(F, sel, device, s);
-    const Flops fl = count_flops(r->fp->sym, &r->p2->sel);
+    r->p2 = so ? phase2_plan_for(F, sel, device, s, env_int("TIB_CRIT_SPLIT_P2", 24)) : phase2_plan_for(F, sel, device, s);
+    // the reference's task model counts the reference's own (natural) order
+    const Closure sel_nat = symbolic_inversion(select_tiles(natural.filled.layout(), natural.filled, req), natural.filled);
+    const Flops fl = count_flops(natural, &sel_nat);
     r->model_flops = fl.total() * count;
     const size_t tile = static_cast<size_t>(r->fp->bp) * r->fp->bp;
     const size_t T = F.size(), C = r->p2->sel.closure.size(), nv = static_cast<size_t>(m->layout.N) * r->fp->bp;
     alloc_factor_stores(r->st, *r->fp, count, device, s, r->p2->flow->host.counters,
                         r->p2->flow->host.scratch_doubles);
     r->A0 = DevBuf(T * tile * count, device, s);
-    for (int k = 0; k < count; ++k) upload_matrix(*ms[k], F, r->fp->bp, r->A0.p + T * tile * k, s);
+    for (int k = 0; k < count; ++k) {
+      if (so) {
+        HostBuf hb(T * tile);
+        permuted_payload(*ms[k], *so, r->fp->bp, hb.p);
+        CK(cudaMemcpyAsync(r->A0.p + T * tile * k, hb.p, T * tile * sizeof(double), cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+      } else {
+        upload_matrix(*ms[k], F, r->fp->bp, r->A0.p + T * tile * k, s);
+      }
+    }
     r->Sg = DevBuf(C * tile * count, device, s);
     r->var = DevBuf(nv * count, device, s);
+    if (so) {
+      r->unperm = std::make_unique<Unpermute>(*r->split, device, s);
+      r->Sn = DevBuf(C * tile, device, s);
+      r->varn = DevBuf(nv, device, s);
+    }
     for (int k = 0; k < count; ++k)
       r->tables.push_back(make_table(r->st.A.p + T * tile * k, r->st.L.p + T * tile * k, r->st.P1.p + T * tile * k,
                                      r->Sg.p + C * tile * k, r->var.p + nv * k,
@@ -1845,6 +2254,7 @@ int tib_resident_run(tib_resident r, int reps, double* ms_total, double* ms_fact
       factor_sweep(*r->fp, r->st, s, r->tables);
       CK(cudaEventRecord(ev[3 * it + 1], s));
       phase2_sweep(*r->p2, s, r->tables);
+      if (r->unperm) r->unperm->run(r->Sg.p, r->Sn.p, r->var.p, r->varn.p, r->fp->bp, s);
       CK(cudaEventRecord(ev[3 * it + 2], s));
     }
     CK(cudaEventSynchronize(ev.back()));

@@ -77,7 +77,7 @@ struct Builder {
   }
   // Splits the emission order into the two queues; returns the global order
   // expressed in final task indices.
-  std::vector<int> finish(int crit_workers, bool chain = false) {
+  std::vector<int> finish(int crit_workers, bool chain = false, int split = -1) {
     // dependency check in emission order (before any restructuring)
     P.tasks = all;
     std::vector<int> ident(all.size());
@@ -99,15 +99,28 @@ struct Builder {
           rq.push_back(queue[i]);
         }
       }
-      DTask c{};
-      c.poll = -1;
-      c.kind = kChainTask;
-      c.c_store = c.c0_store = c.cm_store = c.diag_store = kStoreNone;
-      c.seg_begin = 0;
-      c.seg_count = static_cast<int>(P.chain.size());
+      // one chain task per elimination chain: steps of columns < split, then
+      // the rest (the leaves are emitted in column order)
+      std::vector<int> bounds{0};
+      if (split > 0) {
+        int k = 0;
+        while (k < static_cast<int>(P.chain.size()) && P.chain[static_cast<size_t>(k)].n0 / P.L.b < split) ++k;
+        if (k > 0 && k < static_cast<int>(P.chain.size())) bounds.push_back(k);
+      }
+      bounds.push_back(static_cast<int>(P.chain.size()));
+      const int nchains = P.chain.empty() ? 0 : static_cast<int>(bounds.size()) - 1;
+      if (nchains > 1)
+        for (int& x : conv)
+          if (x >= 0) x += nchains - 1;
       all.clear();
       queue.clear();
-      if (!P.chain.empty()) {
+      for (int q = 0; q < nchains; ++q) {
+        DTask c{};
+        c.poll = -1;
+        c.kind = kChainTask;
+        c.c_store = c.c0_store = c.cm_store = c.diag_store = kStoreNone;
+        c.seg_begin = bounds[static_cast<size_t>(q)];
+        c.seg_count = bounds[static_cast<size_t>(q) + 1] - bounds[static_cast<size_t>(q)];
         all.push_back(c);
         queue.push_back(0);
       }
@@ -117,6 +130,7 @@ struct Builder {
       // is the block's leaf and no other column updates the block in between
       // (the leaf's dependency value is the count this step's signal reaches)
       for (size_t s = 0; s + 1 < P.chain.size(); ++s) {
+        if (std::find(bounds.begin(), bounds.end(), static_cast<int>(s) + 1) != bounds.end()) continue;
         DTask& c0 = P.chain[s];
         const DTask& c1 = P.chain[s + 1];
         if (!(c0.mode & 4) || c1.dep_count < 1) continue;
@@ -208,7 +222,7 @@ void validate_dataflow(const DataflowPlan& plan, const std::vector<int>& order) 
 }
 
 DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer_w, bool fat_leaf, bool chain,
-                                   bool boundary) {
+                                   bool boundary, int split) {
   if (chain) fat_leaf = true;
   if (boundary) fat_leaf = true;
   DataflowPlan P;
@@ -263,7 +277,11 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
   P.upl = cUpl;
   P.counters = cEnd;
   const size_t t_doubles = static_cast<size_t>(N) * bp * bp;
-  P.scratch_doubles = t_doubles + static_cast<size_t>(kRing) * slots_per_col * kB * kB;
+  // one ring per elimination chain (columns [0, split) and [split, N)): the
+  // chains run concurrently, so a column must not wait for a column of the
+  // other chain to release its slots
+  const bool two = split > 0 && split < N;
+  P.scratch_doubles = t_doubles + static_cast<size_t>(two ? 2 : 1) * kRing * slots_per_col * kB * kB;
   P.logdet_doubles = static_cast<size_t>(N) * nb;
   auto aord = [&](long s, int p, int q) { return static_cast<int>(cAord + s * NB2 + p * nb + q); };
   auto afin = [&](long s) { return static_cast<int>(cAfin + s); };
@@ -283,7 +301,9 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
   // the column's scratch ring slots
   auto ringdone = [&](int j) { return static_cast<int>(cRing + j); };
   // ring slot of column j (columns kRing apart share one)
-  auto ring_of = [&](int j) { return static_cast<long long>(j % kRing); };
+  auto ring_of = [&](int j) {
+    return static_cast<long long>(two && j >= split ? kRing + (j - split) % kRing : j % kRing);
+  };
   const int xdone = nb * (nb + 1) / 2;
   const long long tsz = static_cast<long long>(bp) * bp;
 
@@ -714,7 +734,8 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
       }
       ring_count[static_cast<size_t>(j)] = static_cast<int>(groups.size()) + (bnd_col ? 1 : 0);
       const int prev = j - kRing;
-      if (prev >= 0 && ring_count[static_cast<size_t>(prev)] > 0)
+      const bool same_chain = !(two && j >= split && prev < split);
+      if (prev >= 0 && same_chain && ring_count[static_cast<size_t>(prev)] > 0)
         for (size_t x = col_first; x < B.all.size(); ++x) {
           DTask& t = B.all[x];
           const bool writer = t.kind == kSplitTask || (t.kind == kGemmTask && t.c_store == kStoreScratch &&
@@ -728,19 +749,15 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
   // streamed upload: each task polls the upload counter of the latest tile
   // column of A it reads or writes
   {
-    // upload order: column c by the first column k whose elimination reads or
-    // updates one of its tiles (i, c) -- min k < c with (i, k) and (c, k) in F
-    // (the diagonal tile: any k with (c, k) in F), else c
+    // upload order: column c by the first elimination step that touches it --
+    // step k reads column k and updates the tiles (r, c) of every c with
+    // (c, k) in F -- where the steps of the two chains (split) run side by
+    // side: step k comes at time k, or k - split in the second chain
     std::vector<int> first(static_cast<size_t>(N));
-    {
-      std::vector<int> row_min(static_cast<size_t>(N), N);  // smallest column of each tile row
-      for (const Coord& c : F.tiles()) row_min[static_cast<size_t>(c.i)] = std::min(row_min[static_cast<size_t>(c.i)], c.j);
-      for (int c = 0; c < N; ++c) {
-        int k = std::min(c, row_min[static_cast<size_t>(c)]);
-        for (const int* r = F.rows_begin(c); r != F.rows_end(c); ++r) k = std::min(k, std::max(row_min[static_cast<size_t>(*r)], row_min[static_cast<size_t>(c)]));
-        first[static_cast<size_t>(c)] = k;
-      }
-    }
+    auto when = [&](int k) { return two && k >= split ? k - split : k; };
+    for (int c = 0; c < N; ++c) first[static_cast<size_t>(c)] = when(c);
+    for (const Coord& t : F.tiles())
+      if (t.i > t.j) first[static_cast<size_t>(t.i)] = std::min(first[static_cast<size_t>(t.i)], when(t.j));
     P.upload_order.resize(static_cast<size_t>(N));
     for (int c = 0; c < N; ++c) P.upload_order[static_cast<size_t>(c)] = c;
     std::stable_sort(P.upload_order.begin(), P.upload_order.end(),
@@ -768,7 +785,7 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
       t.poll = c >= 0 ? static_cast<int>(cUpl + c) : -1;
     }
   }
-  B.finish(crit_workers, chain);
+  B.finish(crit_workers, chain, two ? split : -1);
   return P;
 }
 

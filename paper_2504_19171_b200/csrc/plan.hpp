@@ -58,8 +58,11 @@ struct DataflowPlan {
 // chain: the leaves (fat) become the steps of one persistent chain task per matrix.
 // boundary: the last leaf of each tile also forms row 0 of the next tile's last
 // panel block and the last update term of the next diagonal block (S trick).
+// split > 0: columns [split, N) form a second elimination chain independent of
+// [0, split) until they meet (two_chain_order): two chain tasks, one scratch
+// ring each.
 DataflowPlan build_factor_dataflow(const Pattern& filled, int crit_workers, int defer_w, bool fat_leaf,
-                                   bool chain = false, bool boundary = false);
+                                   bool chain = false, bool boundary = false, int split = -1);
 
 // Phase 1 alone (selinv.cpp:195-237) from a given factor L (a factor read back
 // from a tile file): X_j = L_jj^{-1} and W_kj = L_kj X_j, every column

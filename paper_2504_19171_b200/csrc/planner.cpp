@@ -569,4 +569,51 @@ std::string write_matrix_market(const HostMatrix& m) {
   return out;
 }
 
+// Two-chain elimination order (planner.hpp).  Admissible when the pattern is a
+// band of s >= 1 tiles plus trailing full arrow rows, only the last tile is
+// partial (it stays last: with no arrow a partial last tile is kept as a
+// one-tile arrow, and the fill check below decides), each interior has at
+// least s columns, and the permuted pattern fills in nothing.
+SplitOrder two_chain_order(const Pattern& F) {
+  SplitOrder so;
+  const Layout& L = F.layout();
+  const int N = L.N;
+  if (N < 4 || !F.has_all_diagonals()) return so;
+  std::vector<int> per_row(static_cast<size_t>(N), 0);
+  for (const Coord& c : F.tiles()) ++per_row[static_cast<size_t>(c.i)];
+  int na = 0;
+  while (na < N - 1 && per_row[static_cast<size_t>(N - 1 - na)] == N - na) ++na;
+  if (na == 0 && L.n % L.b != 0) na = 1;
+  const int M = N - na;
+  int s = 0;
+  for (const Coord& c : F.tiles())
+    if (c.i < M) s = std::max(s, c.i - c.j);
+  if (s < 1 || M < 3 * s + 2) return so;
+  const int h = (M - s) / 2;
+  so.order.reserve(static_cast<size_t>(N));
+  for (int j = 0; j < h; ++j) so.order.push_back(j);
+  for (int j = M - 1; j >= h + s; --j) so.order.push_back(j);
+  for (int j = h; j < h + s; ++j) so.order.push_back(j);
+  for (int j = M; j < N; ++j) so.order.push_back(j);
+  so.pos.assign(static_cast<size_t>(N), 0);
+  for (int k = 0; k < N; ++k) so.pos[static_cast<size_t>(so.order[static_cast<size_t>(k)])] = k;
+  std::vector<Coord> tiles;
+  tiles.reserve(F.size());
+  for (const Coord& c : F.tiles()) {
+    const int a = so.pos[static_cast<size_t>(c.i)], b = so.pos[static_cast<size_t>(c.j)];
+    tiles.push_back(a >= b ? Coord{a, b} : Coord{b, a});
+  }
+  Pattern P(L, std::move(tiles));
+  Pattern filled = symbolic_fill(P);
+  if (filled.size() != F.size()) {
+    so.order.clear();
+    so.pos.clear();
+    return so;
+  }
+  so.permuted = std::move(filled);
+  so.split = h;
+  return so;
+}
+
 }  // namespace tib
+

@@ -166,6 +166,30 @@ void for_each_request_entry(const Layout& L, const Pattern& closure,
 
 uint64_t fnv1a_keys(const std::vector<Coord>& tiles);
 
+// ---- two-chain elimination order (the device's single-matrix path) ----------
+// The reference eliminates tile columns 0 .. N-1, one sequential chain of
+// diagonal factorizations.  For a band + arrow tile pattern (band width s
+// tiles, arrow = the trailing full tile rows) the order
+//     [I_0 ascending, I_1 descending, S, arrow]
+// with I_0 = [0, h), S = [h, h + s), I_1 = [h + s, M) (M = band columns) has
+// two independent chains -- I_1 eliminated from its far end meets the
+// separator S last, like I_0 -- and, at tile granularity, no fill beyond the
+// matrix's own (checked symbolically).  order[k] = original tile of position
+// k; split = first position of the second chain (I_1 then S then arrow).
+struct SplitOrder {
+  std::vector<int> order, pos;  // pos = inverse permutation
+  int split = -1;               // -1: no admissible split
+  Pattern permuted;             // the filled pattern in the new order
+};
+SplitOrder two_chain_order(const Pattern& filled);
+// Tile (i, j) of the permuted matrix (i >= j) -> original tile and whether the
+// stored original tile is its transpose.
+inline Coord split_source(const SplitOrder& so, int i, int j, bool& transposed) {
+  const int a = so.order[static_cast<size_t>(i)], b = so.order[static_cast<size_t>(j)];
+  transposed = a < b;
+  return transposed ? Coord{b, a} : Coord{a, b};
+}
+
 // ---- task-graph / complexity analyzer (dag.cpp; reference dag.hpp:12-77) ------
 struct DagNode {
   int kind = 0;  // 0 TRSM_INV, 1 TRMM, 2 LAUUM, 3 GEMM (the reference's rank order)

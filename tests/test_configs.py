@@ -106,21 +106,25 @@ def test_single_matrix_config_vs_reference(tib, name):
 
 
 @pytest.mark.gpu
-def test_batch_config_vs_reference(tib):
+def test_batch_config_vs_reference(tib, monkeypatch):
     """BASELINE config 5 as one batched call: 64 device-generated matrices;
     the first and last members against the reference's own runs."""
     ms = [tib.generate(50000, 500, 50, 1.0, seed=1000 + k, tile_size=128, device=0) for k in range(64)]
     logdet, diag = tib.selected_inverse_batch(ms)
     for k, name in ((0, "batch1000"), (63, "batch1063")):
         check_against_golden(golden(name), 50000, 128, diag[k], logdet[k], None, None, None)
-    # members are independent: one member alone gives the same bits
+    # members are independent: one member alone (in the natural elimination
+    # order, like the batch) gives the same bits
+    monkeypatch.setenv("TIB_SPLIT", "0")
     single = tib.selected_inverse(ms[63], "pattern")
     assert single.logdet() == logdet[63]
     assert np.array_equal(single.diagonal(), diag[63])
 
 
 @pytest.mark.gpu
-def test_device_generator_is_bitwise_the_host_generator(tib):
+def test_device_generator_is_bitwise_the_host_generator(tib, monkeypatch):
+    # (one elimination order for both: host matrices may stream in the natural one)
+    monkeypatch.setenv("TIB_SPLIT", "0")
     for args in ((10000, 200, 50, 42, 128), (5000, 0, 700, 3, 96), (3000, 400, 0, 9, 100), (777, 50, 30, 1, 64)):
         n, w, t, seed, b = args
         h = tib.generate(n, w, t, 1.0, seed=seed, tile_size=b)

@@ -114,7 +114,7 @@ def test_small_config_vs_reference(tib, orc):
     print(f"elementwise max_rel_error (information only): {info:.3e}")
 
 
-def test_factor_path_and_determinism(tib, orc):
+def test_factor_path_and_determinism(tib, orc, monkeypatch):
     n, w, t, d, seed, b = 3000, 300, 40, 1.0, 17, 128
     m = tib.generate(n, w, t, d, seed=seed, tile_size=b)
     f = tib.factorize(m, workers=2)
@@ -125,10 +125,15 @@ def test_factor_path_and_determinism(tib, orc):
     assert normwise(P1, ref["phase1"]) <= TOL
     assert abs(f.logdet() - ref["logdet"]) <= TOL * abs(ref["logdet"])
     via = tib.selected_inverse_of_factor(f, "pattern")
+    monkeypatch.setenv("TIB_SPLIT_STREAMED", "1")  # the two-chain order, streamed
     direct = tib.selected_inverse(m, "pattern")
     again = tib.selected_inverse(m, "pattern")
     # fixed accumulation order, no atomics on data: bitwise reproducible
-    assert direct.checksum == again.checksum == via.checksum
+    assert direct.checksum == again.checksum
+    assert normwise(direct.tiles()[2], via.tiles()[2]) <= 1e-13
+    # the natural elimination order is the factor's: the same bits
+    monkeypatch.setenv("TIB_SPLIT", "0")
+    assert tib.selected_inverse(m, "pattern").checksum == via.checksum
     assert f.checksum == tib.factorize(m).checksum
     # one factor serves several requests (module.cpp:208-215)
     diag = tib.selected_inverse_of_factor(f, "diagonal")
@@ -137,7 +142,8 @@ def test_factor_path_and_determinism(tib, orc):
 
 @pytest.mark.parametrize("count", [3, 6, 80])  # 6 > TIB_DEDICATE_MAX_BATCH: chains share their SMs;
 # 80 > the reserved critical workers: every chain still runs on its own worker
-def test_batch_matches_single(tib, count):
+def test_batch_matches_single(tib, count, monkeypatch):
+    monkeypatch.setenv("TIB_SPLIT", "0")  # single calls in the batch's (natural) elimination order
     b = 256 if count > 6 else 128
     ms = [tib.generate(5000, 500, 50, 1.0, seed=1000 + k, tile_size=b) for k in range(count)]
     logdet, diag = tib.selected_inverse_batch(ms)
@@ -147,9 +153,13 @@ def test_batch_matches_single(tib, count):
         assert np.array_equal(diag[k], res.diagonal())
 
 
-def test_streamed_upload_is_bitwise_identical(tib, monkeypatch):
+@pytest.mark.parametrize("split", ["0", "1"])
+def test_streamed_upload_is_bitwise_identical(tib, monkeypatch, split):
     """The public path streams A up column by column under the factor sweep
-    (tasks poll per-column upload counters); the result must not depend on it."""
+    (tasks poll per-column upload counters); the result must not depend on it,
+    in either elimination order."""
+    monkeypatch.setenv("TIB_SPLIT", split)
+    monkeypatch.setenv("TIB_SPLIT_STREAMED", split)
     m = tib.generate(6000, 700, 60, 1.0, seed=23, tile_size=256)
     streamed = tib.selected_inverse(m, "pattern")
     monkeypatch.setenv("TIB_STREAM_UPLOAD", "0")
@@ -158,10 +168,64 @@ def test_streamed_upload_is_bitwise_identical(tib, monkeypatch):
     assert streamed.logdet() == upfront.logdet()
 
 
+@pytest.mark.parametrize("how", ["streamed", "upfront", "device"])
+def test_two_chain_order_matches_natural(tib, orc, monkeypatch, how):
+    """Single-matrix calls run in the two-chain elimination order (interior 1
+    reversed, separator, arrow) with Sigma un-permuted on the
+    device: Sigma, the marginal variances and the logdet equal the natural
+    order's (and the oracle's) to rounding, for every upload path."""
+    n, w, t, seed, b = 9000, 600, 70, 31, 128
+    m = tib.generate(n, w, t, 1.0, seed=seed, tile_size=b, device=0 if how == "device" else None)
+    assert tib.two_chain_order(m)[1] > 0
+    if how == "upfront":
+        monkeypatch.setenv("TIB_STREAM_UPLOAD", "0")
+    if how == "streamed":  # host inputs stream in the natural order unless asked
+        monkeypatch.setenv("TIB_SPLIT_STREAMED", "1")
+    got = tib.selected_inverse(m, "pattern")
+    monkeypatch.setenv("TIB_SPLIT", "0")
+    nat = tib.selected_inverse(m, "pattern")
+    assert got.checksum != nat.checksum  # (the two orders round differently: the split path ran)
+    ti, tj, pay = got.tiles()
+    ti2, tj2, pay2 = nat.tiles()
+    assert np.array_equal(ti, ti2) and np.array_equal(tj, tj2)
+    assert normwise(pay, pay2) <= 1e-13
+    assert elementwise(got.diagonal(), nat.diagonal()) <= 1e-12
+    assert abs(got.logdet() - nat.logdet()) <= 1e-13 * abs(nat.logdet())
+    ref = orc.selected_inverse_generated(n, w, t, 1.0, seed, b, "pattern")
+    assert normwise(pay, ref["payload"]) <= TOL
+    assert elementwise(got.diagonal(), ref["diag"]) <= TOL
+    # exactly symmetric diagonal tiles survive the un-permutation
+    for k in np.nonzero(ti == tj)[0][:8]:
+        assert np.array_equal(pay[k], pay[k].T)
+    # entries in the reference's order, like the natural call
+    r1, c1, v1 = got.entries_arrays()
+    r2, c2, v2 = nat.entries_arrays()
+    assert np.array_equal(r1, r2) and np.array_equal(c1, c2)
+    assert normwise(v1, v2) <= 1e-13
+
+
+def test_two_chain_not_spd_reports_the_natural_pivot(tib):
+    """A NotSpd in the permuted elimination is re-run in the natural order, so
+    the error carries the reference's first non-positive pivot."""
+    m = tib.generate(6000, 500, 40, 1.0, seed=3, tile_size=128)
+    ti, tj, pay = m.tiles()
+    pay = pay.copy()
+    k = int(np.nonzero((ti == tj) & (ti == 30))[0][0])
+    pay[k][5, 5] = -1.0
+    bad = tib.from_tiles(m.n, 128, ti, tj, pay)
+    assert tib.two_chain_order(bad)[1] > 0
+    with pytest.raises(tib.NotSpdError) as e:
+        tib.selected_inverse(bad, "pattern")
+    with pytest.raises(tib.NotSpdError) as e2:
+        tib.factorize(bad)
+    assert (e.value.pivot, e.value.tile_i) == (e2.value.pivot, e2.value.tile_i)
+
+
 def test_diagonal_tiles_lower_triangle_only(tib, monkeypatch):
     """Diagonal tiles of A are significant in their lower triangle only (the
     reference's potrf reads the lower part, kernels.cpp:48-69): garbage in the
     strict upper part changes nothing, streamed upload or not."""
+    monkeypatch.setenv("TIB_SPLIT", "0")  # the same elimination order for both uploads
     m = tib.generate(6000, 700, 60, 1.0, seed=29, tile_size=128)
     ti, tj, pay = m.tiles()
     ref = tib.selected_inverse(m, "pattern")

@@ -1,5 +1,5 @@
-"""One public selected_inverse call on a device-generated large matrix (for an
-ncu launch list of the generator kernels next to the sweeps)."""
+"""Public selected_inverse calls on a device-generated large matrix (for an
+ncu launch list of the generator / permutation kernels next to the sweeps)."""
 import sys
 import time
 
@@ -12,3 +12,4 @@ for rep in range(int(sys.argv[1]) if len(sys.argv) > 1 else 1):
     r = tib.selected_inverse(m, "pattern", device=0)
     r.diagonal()
     print(f"rep {rep}: {1e3 * (time.perf_counter() - t0):.1f} ms", flush=True)
+    del r
