@@ -337,9 +337,10 @@ static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int 
 }
 
 static std::shared_ptr<Phase2Plan> phase2_plan_for(const Pattern& F, const Closure& sel, int device,
-                                                   cudaStream_t s, int crit = -1) {
+                                                   cudaStream_t s, int crit = -1, int split = -1) {
   if (crit < 0) crit = crit_workers(false);
-  const uint64_t key = pattern_hash(sel.closure, pattern_hash(F, 2 + 7919ull * static_cast<uint64_t>(crit)));
+  const uint64_t key = pattern_hash(
+      sel.closure, pattern_hash(F, 2 + 7919ull * static_cast<uint64_t>(crit) + 104729ull * static_cast<uint64_t>(split + 2)));
   {
     std::lock_guard<std::mutex> lk(g_plan_mu);
     auto it = g_p2plans.find({device, key});
@@ -347,7 +348,7 @@ static std::shared_ptr<Phase2Plan> phase2_plan_for(const Pattern& F, const Closu
   }
   auto plan = std::make_shared<Phase2Plan>();
   plan->sel = sel;
-  plan->flow = upload_plan(build_phase2_dataflow(F, plan->sel, crit), device, s);
+  plan->flow = upload_plan(build_phase2_dataflow(F, plan->sel, crit, split), device, s);
   plan->flow->crit_batch = crit_workers_batch(false);
   plan->flow->c0_prefetch = env_int("TIB_C0_PF_P2", 1);
   plan->bp = plan->flow->host.bp;
@@ -993,7 +994,7 @@ static SigmaObj* selected_inverse_split(const MatrixObj& m, const Request& req, 
   Request preq;
   preq.preset = kFactorPattern;
   const Closure selp = symbolic_inversion(select_tiles(Fp.layout(), Fp, preq), Fp);
-  auto p2 = phase2_plan_for(Fp, selp, device, s, env_int("TIB_CRIT_SPLIT_P2", 24));
+  auto p2 = phase2_plan_for(Fp, selp, device, s, env_int("TIB_CRIT_SPLIT_P2", 24), sc.so.split);
   tm.mark("plans");
   const int bp = fp->bp, N = m.layout.N;
   const size_t bb = static_cast<size_t>(bp) * bp, T = Fp.size();
@@ -2129,7 +2130,7 @@ int tib_plan_export(tib_matrix m, int preset, const long* rows, const long* cols
     } else {
       const Closure sel =
           symbolic_inversion(select_tiles(sym.filled.layout(), sym.filled, make_request(preset, rows, cols, ne)), sym.filled);
-      P = build_phase2_dataflow(sym.filled, sel, crit_workers);
+      P = build_phase2_dataflow(sym.filled, sel, crit_workers, split);
     }
     if (sizes) {
       sizes[0] = static_cast<double>(P.tasks.size());
@@ -2202,7 +2203,8 @@ int tib_resident_create_batch(const tib_matrix* ms, int count, int device, tib_r
     r->fp = so ? factor_plan_for(so->permuted, device, s, so->split) : factor_plan_for(m->pattern, device, s);
     const Pattern& F = r->fp->sym.filled;
     const Closure sel = symbolic_inversion(select_tiles(F.layout(), F, req), F);
-    r->p2 = so ? phase2_plan_for(F, sel, device, s, env_int("TIB_CRIT_SPLIT_P2", 24)) : phase2_plan_for(F, sel, device, s);
+    r->p2 = so ? phase2_plan_for(F, sel, device, s, env_int("TIB_CRIT_SPLIT_P2", 24), so->split)
+               : phase2_plan_for(F, sel, device, s);
     // the reference's task model counts the reference's own (natural) order
     const Closure sel_nat = symbolic_inversion(select_tiles(natural.filled.layout(), natural.filled, req), natural.filled);
     const Flops fl = count_flops(natural, &sel_nat);

@@ -871,7 +871,7 @@ DataflowPlan build_phase1_dataflow(const Pattern& F) {
   return P;
 }
 
-DataflowPlan build_phase2_dataflow(const Pattern& F, const Closure& sel, int crit_workers) {
+DataflowPlan build_phase2_dataflow(const Pattern& F, const Closure& sel, int crit_workers, int split) {
   DataflowPlan P;
   P.L = F.layout();
   const int bp = (P.L.b + kB - 1) / kB * kB, nb = bp / kB, NB2 = nb * nb;
@@ -907,7 +907,12 @@ DataflowPlan build_phase2_dataflow(const Pattern& F, const Closure& sel, int cri
   const int slots_per_col = *std::max_element(col_slots.begin(), col_slots.end());
   const long cSpart = 0, cSfin = cSpart + Tc * NB2, cArrive = cSfin + Tc;
   P.counters = cArrive + static_cast<long>(N) * slots_per_col;
-  P.scratch_doubles = static_cast<size_t>(kRing) * slots_per_col * kB * kB;
+  // two-chain order (split > 0): the columns below the split are a second,
+  // independent chain once the columns above are done -- its own ring, so
+  // it does not wait for the other chain's columns to release slots
+  const bool two = split > 0 && split < N;
+  P.scratch_doubles = static_cast<size_t>(two ? 2 : 1) * kRing * slots_per_col * kB * kB;
+  auto ring_slot = [&](int i) { return two && i < split ? kRing + i % kRing : i % kRing; };
   auto spart = [&](long s, int p, int q) { return static_cast<int>(cSpart + s * NB2 + p * nb + q); };
   auto sfin = [&](long s) { return static_cast<int>(cSfin + s); };
   auto cslot = [&](int i, int j) {
@@ -932,13 +937,24 @@ DataflowPlan build_phase2_dataflow(const Pattern& F, const Closure& sel, int cri
     const int i = cw.col;
     const std::vector<int>& K = Kof[static_cast<size_t>(i)];
     const int kcrit = K.empty() ? -1 : K[0];
-    // ring release: the column processed kRing steps earlier must be complete
+    // ring release: the column processed kRing steps earlier on the same ring
+    // must be complete
     std::vector<Dep> ring_deps;
-    if (ci >= static_cast<size_t>(kRing)) ring_deps = col_done[static_cast<size_t>(sel.columns[ci - kRing].col)];
+    {
+      int seen = 0;
+      for (size_t cj = ci; cj-- > 0;) {
+        const int pc = sel.columns[cj].col;
+        if (two && ((pc < split) != (i < split))) continue;
+        if (++seen == kRing) {
+          ring_deps = col_done[static_cast<size_t>(pc)];
+          break;
+        }
+      }
+    }
     int slot_next = 0;
     auto take = [&](int parts, DTask& t, int part, int base) {
       t.kind = kSplitTask;
-      t.p_off = (static_cast<long long>(i % kRing) * slots_per_col + base) * kB * kB;
+      t.p_off = (static_cast<long long>(ring_slot(i)) * slots_per_col + base) * kB * kB;
       t.aux0 = static_cast<int>(cArrive + static_cast<long>(i) * slots_per_col + base);
       t.aux1 = (part << 8) | parts;
     };

@@ -73,7 +73,9 @@ DataflowPlan build_phase1_dataflow(const Pattern& filled);
 // Phase 2 over a closure: per column descending, off-diagonal targets split
 // into an early part and the k == j term, diagonal targets into LAUUM + early
 // terms and the first-row term; the first-row chain is queue 0.
-DataflowPlan build_phase2_dataflow(const Pattern& filled, const Closure& sel, int crit_workers);
+// split > 0 (two-chain order): the columns below split get their own ring of
+// split-K slots (an independent chain once the columns above are done).
+DataflowPlan build_phase2_dataflow(const Pattern& filled, const Closure& sel, int crit_workers, int split = -1);
 
 // Simulates the plan in its global emission order (queue 0 and queue 1 are
 // both subsequences of it) and throws ConsistencyError if any dependency is

@@ -192,7 +192,7 @@ def run_plans(tib, matrix, selection, order=None, split=-1):
     fpat = tib.factor_pattern(matrix)
     closure, _ = tib.closure_tiles(matrix, selection)
     pf = tib.plan_export(matrix, selection, 0, crit_workers=1, split=split)
-    pp = tib.plan_export(matrix, selection, 1, crit_workers=1)
+    pp = tib.plan_export(matrix, selection, 1, crit_workers=1, split=split)
     bp, b, n = pf["bp"], matrix.tile_size, matrix.n
     N = matrix.n_tiles
     nb = bp // BLK
