@@ -638,20 +638,34 @@ struct MatrixObj {
 
 // Generator on the device (generate.cu) into a tile store over `pat` with row
 // stride bp (identity padding), stream-ordered.
-static void device_generate(const MatrixObj& m, const Pattern& pat, int bp, double* out, cudaStream_t s) {
+// A batch of device-generated matrices with the same parameters but their own
+// seeds (ms[k]'s store at out + k * stride) is one launch per kernel.
+static void device_generate(const std::vector<const MatrixObj*>& ms, const Pattern& pat, int bp, double* out,
+                            size_t stride, cudaStream_t s) {
+  const MatrixObj& m = *ms[0];
   const int N = pat.layout().N;
   std::vector<int> meta(static_cast<size_t>(N) + 1 + pat.size());  // colptr (N + 1), then rows
   int maxc = 0;
   for (int j = 0; j <= N; ++j) meta[static_cast<size_t>(j)] = static_cast<int>(pat.col_start(j));
   for (int j = 0; j < N; ++j) maxc = std::max(maxc, static_cast<int>(pat.col_start(j + 1) - pat.col_start(j)));
   for (size_t k = 0; k < pat.size(); ++k) meta[static_cast<size_t>(N) + 1 + k] = pat.tiles()[k].i;
+  std::vector<unsigned long long> seeds;
+  for (const MatrixObj* x : ms) seeds.push_back(x->gen.seed);
   int* d_meta = nullptr;
+  unsigned long long* d_seeds = nullptr;
   CK(cudaMallocAsync(reinterpret_cast<void**>(&d_meta), meta.size() * sizeof(int), s));
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&d_seeds), seeds.size() * sizeof(unsigned long long), s));
   CK(cudaMemcpyAsync(d_meta, meta.data(), meta.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_seeds, seeds.data(), seeds.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
   CK(static_cast<cudaError_t>(launch_generate_arrowhead(m.gen.n, m.gen.w, m.gen.t, m.gen.seed, m.layout.b, bp, N,
-                                                        d_meta, d_meta + N + 1, maxc, out, s)));
+                                                        d_meta, d_meta + N + 1, maxc, out, s, d_seeds,
+                                                        static_cast<int>(ms.size()), static_cast<long long>(stride))));
   CK(cudaFreeAsync(d_meta, s));
-  CK(cudaStreamSynchronize(s));  // the host vector above dies with this scope
+  CK(cudaFreeAsync(d_seeds, s));
+  CK(cudaStreamSynchronize(s));  // the host vectors above die with this scope
+}
+static void device_generate(const MatrixObj& m, const Pattern& pat, int bp, double* out, cudaStream_t s) {
+  device_generate(std::vector<const MatrixObj*>{&m}, pat, bp, out, 0, s);
 }
 
 static DeviceRt& runtime(int device);
@@ -1886,7 +1900,9 @@ int tib_sigma_entries(tib_sigma sg, long* count, long* rows, long* cols, double*
     const Pattern& C = sg->plan->sel.closure;
     const int bp = sg->plan->bp;
     const bool want = rows || cols || vals;
-    const double* h = want ? sigma_host(*sg) : nullptr;
+    // extract_entries order (selinv.cpp:387-439); the values are gathered on
+    // the device unless the request reads a large part of the store anyway
+    std::vector<long long> at;
     long k = 0;
     for_each_request_entry(L, C, sg->plan->sel.requested, sg->req, [&](long r, long c) {
       const Address a = map_entry_to_tile(L, r, c);
@@ -1898,11 +1914,24 @@ int tib_sigma_entries(tib_sigma sg, long* count, long* rows, long* cols, double*
         if (rows) rows[k] = r;
         if (cols) cols[k] = c;
         if (vals)
-          vals[k] = h[static_cast<size_t>(slot) * bp * bp + static_cast<size_t>(a.row_off) * bp + a.col_off];
+          at.push_back(static_cast<long long>(slot) * bp * bp + static_cast<long long>(a.row_off) * bp + a.col_off);
       }
       ++k;
     });
     *count = k;
+    if (!vals || at.empty()) return;
+    if (sg->host || at.size() * 16 > sg->S.n) {  // (or already on the host)
+      const double* h = sigma_host(*sg);
+      for (size_t e = 0; e < at.size(); ++e) vals[e] = h[at[e]];
+      return;
+    }
+    DeviceRt& rt = runtime(sg->device);
+    DevBuf idx((at.size() + 0), sg->device, rt.stream), out(at.size(), sg->device, rt.stream);
+    CK(cudaMemcpyAsync(idx.p, at.data(), at.size() * sizeof(long long), cudaMemcpyHostToDevice, rt.stream));
+    launch_gather(sg->S.p, reinterpret_cast<const long long*>(idx.p), out.p, static_cast<long long>(at.size()), rt.stream);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(vals, out.p, at.size() * sizeof(double), cudaMemcpyDeviceToHost, rt.stream));
+    CK(cudaStreamSynchronize(rt.stream));
   });
 }
 int tib_sigma_tiles(tib_sigma sg, int* ti, int* tj, double* payload) {
@@ -1974,8 +2003,17 @@ int tib_selected_inverse_batch(const tib_matrix* ms, int count, int device, doub
     const bool pipelined = host_ready && F == m0.pattern && pipe > 0 && count > pipe;
     bool stream_up = !pipelined && host_ready && env_int("TIB_STREAM_UPLOAD", 1) != 0 && fp->flow->host.upl >= 0 &&
                      static_cast<size_t>(count) <= max_batch(*fp->flow);
+    // device-generated members with one parameter set: one generator launch
+    bool gen_all = !stream_up && !pipelined;
+    for (int k = 0; k < count && gen_all; ++k)
+      gen_all = ms[k]->gen.on && ms[k]->gen.n == m0.gen.n && ms[k]->gen.w == m0.gen.w && ms[k]->gen.t == m0.gen.t;
+    if (gen_all) {
+      std::vector<const MatrixObj*> mm;
+      for (int k = 0; k < count; ++k) mm.push_back(ms[k]);
+      device_generate(mm, F, fp->bp, st.A.p, T * tile, s);
+    }
     for (int k = 0; k < count; ++k) {
-      if (!stream_up && !pipelined) upload_matrix(*ms[k], F, fp->bp, st.A.p + T * tile * k, s);
+      if (!stream_up && !pipelined && !gen_all) upload_matrix(*ms[k], F, fp->bp, st.A.p + T * tile * k, s);
       tables.push_back(make_table(st.A.p + T * tile * k, st.L.p + T * tile * k, st.P1.p + T * tile * k,
                                   Sg.p + p2->sel.closure.size() * tile * k, var.p + static_cast<size_t>(m0.layout.N) * fp->bp * k,
                                   st.scratch.p + st.scratch_stride * k,

@@ -41,6 +41,10 @@ struct Gen {
   int b, bp, N;
   const int* colptr;  // CSC of the target pattern: slots of tile column j are colptr[j] .. colptr[j+1]-1
   const int* rows;    // tile row of every slot
+  // a batch (one launch): matrix m (the last grid dimension) has seed
+  // seeds[m] and its store at out + m * stride
+  const unsigned long long* seeds;
+  long long stride;
 };
 
 __device__ __forceinline__ double draw_value(unsigned long long state) {
@@ -90,6 +94,10 @@ __device__ __forceinline__ long long slot_of(const Gen& g, int i, int j) {
 }
 
 __global__ void fill_kernel(Gen g, double* __restrict__ out) {
+  if (g.seeds) {
+    g.seed = g.seeds[blockIdx.z];
+    out += blockIdx.z * g.stride;
+  }
   const long long k = blockIdx.x;
   const int J = blockIdx.y;  // tile column (grid.y), slot k = colptr[J] + blockIdx.x
   const int s0 = __ldg(g.colptr + J), s1 = __ldg(g.colptr + J + 1);
@@ -154,6 +162,7 @@ __device__ __forceinline__ double seq_abs_sum(double s, const double* __restrict
 // After fill: diagonal entry x = 1 + sum |v| in draw order, from the stored
 // tiles -- band rows (x < n - t), one thread each.
 __global__ void rowsum_kernel(Gen g, double* __restrict__ out) {
+  out += blockIdx.y * g.stride;
   const long long x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (x >= g.n - g.t) return;
   const long long ab = g.n - g.t;
@@ -192,6 +201,7 @@ __global__ void rowsum_kernel(Gen g, double* __restrict__ out) {
 // additions (an added +0.0 past a chunk's end leaves s >= 0 unchanged), so the
 // same bits, at the FP64 add latency.
 __global__ void arrow_rowsum_kernel(Gen g, double* __restrict__ out) {
+  out += blockIdx.y * g.stride;
   const int lane = threadIdx.x & 31;
   const long long x = g.n - g.t + (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
   if (x >= g.n) return;
@@ -243,12 +253,14 @@ __global__ void arrow_rowsum_kernel(Gen g, double* __restrict__ out) {
 
 // colptr (N + 1) and rows (slots) describe the target pattern in device memory.
 int launch_generate_arrowhead(long n, long w, long t, unsigned long long seed, int b, int bp, int N, const int* colptr,
-                              const int* rows, int max_col_slots, double* out, cudaStream_t s) {
-  const Gen g{n, w, t, seed, b, bp, N, colptr, rows};
+                              const int* rows, int max_col_slots, double* out, cudaStream_t s,
+                              const unsigned long long* seeds, int count, long long stride) {
+  const Gen g{n, w, t, seed, b, bp, N, colptr, rows, seeds, stride};
+  const unsigned nm = static_cast<unsigned>(count > 0 ? count : 1);
   if (N > 0 && max_col_slots > 0)
-    fill_kernel<<<dim3(static_cast<unsigned>(max_col_slots), static_cast<unsigned>(N)), 256, 0, s>>>(g, out);
-  if (n - t > 0) rowsum_kernel<<<static_cast<unsigned>((n - t + 255) / 256), 256, 0, s>>>(g, out);
-  if (t > 0) arrow_rowsum_kernel<<<static_cast<unsigned>((t + 3) / 4), 128, 0, s>>>(g, out);
+    fill_kernel<<<dim3(static_cast<unsigned>(max_col_slots), static_cast<unsigned>(N), nm), 256, 0, s>>>(g, out);
+  if (n - t > 0) rowsum_kernel<<<dim3(static_cast<unsigned>((n - t + 255) / 256), nm), 256, 0, s>>>(g, out);
+  if (t > 0) arrow_rowsum_kernel<<<dim3(static_cast<unsigned>((t + 3) / 4), nm), 128, 0, s>>>(g, out);
   return static_cast<int>(cudaGetLastError());
 }
 

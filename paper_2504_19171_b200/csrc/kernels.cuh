@@ -65,12 +65,14 @@ void launch_dataflow(const FlowArgs& a, const int* need, const int* init0, int n
                      int grid, cudaStream_t s);
 void launch_zero_strips(const ZeroStrip* z, int count, int ld, int batch, const BaseTable* tables, cudaStream_t s);
 void launch_fill(double* p, double v, size_t count, cudaStream_t s);
+void launch_gather(const double* src, const long long* idx, double* out, long long n, cudaStream_t s);
 void launch_permute_tiles(double* dst, const double* src, const int* d, const int* s, const unsigned char* tr,
                           int count, int bp, int max_blocks, cudaStream_t st);
 void launch_permute_rows(double* dst, const double* src, const int* d, const int* s, int count, int bp, cudaStream_t st);
 // generate.cu: density-1 arrowhead generator (matgen.cpp:59-120) into a tile
 // store over a pattern given as device CSC (colptr[N + 1], rows), row stride bp.
 int launch_generate_arrowhead(long n, long w, long t, unsigned long long seed, int b, int bp, int N, const int* colptr,
-                              const int* rows, int max_col_slots, double* out, cudaStream_t s);
+                              const int* rows, int max_col_slots, double* out, cudaStream_t s,
+                              const unsigned long long* seeds = nullptr, int count = 1, long long stride = 0);
 
 }  // namespace tib
