@@ -258,6 +258,16 @@ static int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e && *e ? std::atoi(e) : dflt;
 }
+// Streamed uploads overlap copies on one stream with the persistent sweep on
+// another, the sweep polling for the copies.  A profiler that serialises the
+// device's work (Nsight Compute injects itself through CUDA_INJECTION64_PATH)
+// would hold the copies behind the sweep and stall it until the watchdog
+// fires: then (and with TIB_STREAM_UPLOAD=0) A goes up before the sweep.
+static bool streaming_allowed() {
+  if (env_int("TIB_STREAM_UPLOAD", 1) == 0) return false;
+  const char* inj = std::getenv("CUDA_INJECTION64_PATH");
+  return !(inj && *inj);
+}
 // CTAs reserved for the critical queue: the factor sweep's q0 (the chain's
 // helpers) is heavy and latency-sensitive, phase 2's (diagonal parts) is light
 static int crit_workers(bool factor) {
@@ -1037,7 +1047,7 @@ static SigmaObj* selected_inverse_split(const MatrixObj& m, const Request& req, 
                                        st.status.p, st.ctr(0))};
   std::vector<BaseTable> tp{make_table(st.A.p, st.L.p, st.P1.p, st.A.p, varp.p, st.scratch.p, st.logdet.p,
                                        st.status.p, st.ctr(0))};
-  const bool stream_up = !m.gen.on && bp == m.layout.b && m.payload.pinned && env_int("TIB_STREAM_UPLOAD", 1) != 0 &&
+  const bool stream_up = !m.gen.on && bp == m.layout.b && m.payload.pinned && streaming_allowed() &&
                          fp->flow->host.upl >= 0;
   if (m.gen.on) {
     // natural tiles from the device generator into the staging store, then permuted
@@ -1172,7 +1182,7 @@ static SigmaObj* selected_inverse_matrix(const MatrixObj& m, const Request& req,
   // the sweep waits for the upload in either order, and the split order's
   // chains, twice as fast as the upload, leave tasks polling for columns
   // (large config: 216 vs 203 ms).  TIB_SPLIT_STREAMED=1/0 forces it.
-  const bool streams = !m.gen.on && m.payload.pinned && m.layout.b % 64 == 0 && env_int("TIB_STREAM_UPLOAD", 1) != 0;
+  const bool streams = !m.gen.on && m.payload.pinned && m.layout.b % 64 == 0 && streaming_allowed();
   bool split_ok = !streams;
   if (streams) {
     const int forced = env_int("TIB_SPLIT_STREAMED", -1);
@@ -1208,7 +1218,7 @@ static SigmaObj* selected_inverse_matrix(const MatrixObj& m, const Request& req,
   // when the host tiles already have the device layout (b = bp; fill-in slots
   // are zeroed on the upload stream).
   const bool stream_up = !m.gen.on && fp->bp == m.layout.b && m.payload.pinned &&
-                         env_int("TIB_STREAM_UPLOAD", 1) != 0 && fp->flow->host.upl >= 0;
+                         streaming_allowed() && fp->flow->host.upl >= 0;
   if (!stream_up) upload_matrix(m, F, fp->bp, st.A.p, s);
   auto* res = new SigmaObj;
   std::unique_ptr<SigmaObj> guard(res);
@@ -2001,7 +2011,7 @@ int tib_selected_inverse_batch(const tib_matrix* ms, int count, int device, doub
     // column has not arrived, and the sweep runs after the upload, not under it.
     const int pipe = env_int("TIB_BATCH_PIPE", 16);
     const bool pipelined = host_ready && F == m0.pattern && pipe > 0 && count > pipe;
-    bool stream_up = !pipelined && host_ready && env_int("TIB_STREAM_UPLOAD", 1) != 0 && fp->flow->host.upl >= 0 &&
+    bool stream_up = !pipelined && host_ready && streaming_allowed() && fp->flow->host.upl >= 0 &&
                      static_cast<size_t>(count) <= max_batch(*fp->flow);
     // device-generated members with one parameter set: one generator launch
     bool gen_all = !stream_up && !pipelined;
