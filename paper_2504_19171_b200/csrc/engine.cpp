@@ -254,6 +254,8 @@ struct Phase2Plan {
   int bp = 0, nb = 0;
 };
 
+constexpr int kDeferW = 2;  // phase-1 W tasks of column j are emitted with column j + 2 (bulk filler)
+
 static int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e && *e ? std::atoi(e) : dflt;
@@ -331,9 +333,9 @@ static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int 
   plan->L = plan->sym.filled.layout();
   // two chains keep the critical queue busier per reserved worker (tools/ab_env.py: 24 / 24 best)
   const int crit = split > 0 ? env_int("TIB_CRIT_SPLIT_FACTOR", 24) : crit_workers(true);
-  plan->flow = upload_plan(build_factor_dataflow(plan->sym.filled, crit, env_int("TIB_DEFER_W", 2),
-                                                  env_int("TIB_FAT_LEAF", 0) != 0, env_int("TIB_CHAIN", 1) != 0,
-                                                  env_int("TIB_CHAIN", 1) != 0 && env_int("TIB_BOUNDARY", 1) != 0,
+  // the device sweep: chain task, fat leaves and the tile-boundary trick
+  // always (the combinations the executor is tested with)
+  plan->flow = upload_plan(build_factor_dataflow(plan->sym.filled, crit, kDeferW, true, true, true,
                                                   split),
                            device, s);
   plan->flow->crit_batch = crit_workers_batch(true);
@@ -2173,8 +2175,7 @@ int tib_plan_export(tib_matrix m, int preset, const long* rows, const long* cols
     if (which == 0) {
       // the CPU simulator runs the same decomposition as the GPU chain, with the
       // chain's steps kept as (fat / boundary) leaf tasks
-      P = build_factor_dataflow(sym.filled, crit_workers, env_int("TIB_DEFER_W", 2), env_int("TIB_FAT_LEAF", 0) != 0,
-                                false, env_int("TIB_CHAIN", 1) != 0 && env_int("TIB_BOUNDARY", 1) != 0, split);
+      P = build_factor_dataflow(sym.filled, crit_workers, kDeferW, true, false, true, split);
     } else {
       const Closure sel =
           symbolic_inversion(select_tiles(sym.filled.layout(), sym.filled, make_request(preset, rows, cols, ne)), sym.filled);

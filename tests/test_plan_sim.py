@@ -38,15 +38,6 @@ def test_plan_simulation_matches_oracle(tib, orc, case):
         assert normwise(var, ref["diag"]) <= 1e-12
 
 
-def test_plan_simulation_fat_leaf(tib, orc, monkeypatch):
-    monkeypatch.setenv("TIB_FAT_LEAF", "1")
-    n, w, t, d, seed, b = 520, 150, 20, 1.0, 11, 128
-    m = tib.generate(n, w, t, d, seed=seed, tile_size=b)
-    _, _, sig, logdet, _, _ = run_plans(tib, m, "pattern")
-    ref = orc.selected_inverse_generated(n, w, t, d, seed, b, "pattern")
-    assert normwise(sig, ref["payload"]) <= 1e-12
-
-
 def test_plan_simulation_reports_not_spd(tib):
     a = np.eye(6)
     a[4, 4] = -1.0  # test_cholesky.cpp:161-182: pivot 4, tile (2, 2) at b = 2
