@@ -738,6 +738,7 @@ struct FactorObj {
   double logdet = 0;
 };
 
+struct Unpermute;
 struct SigmaObj {
   int device = 0;
   Layout layout;
@@ -746,6 +747,11 @@ struct SigmaObj {
   DevBuf S, var;
   double logdet = 0;
   std::unique_ptr<HostBuf> host;  // lazily downloaded bp-layout tiles
+  // two-chain order: Sigma and the variances stay in the permuted order (Sp,
+  // var); S is un-permuted on the device the first time a whole-store
+  // accessor needs it, entries and the diagonal are mapped directly
+  std::shared_ptr<const Unpermute> unperm;
+  DevBuf Sp;
 };
 
 static void fill_matrix(MatrixObj& m, HostMatrix&& hm) {
@@ -977,6 +983,8 @@ static DevBuf to_device(const std::vector<T>& v, int dev, cudaStream_t s) {
 struct Unpermute {
   DevBuf d, src, tr, rd, rs;
   int count = 0, N = 0;
+  std::vector<int> slot_of, pos;            // natural closure slot -> permuted slot; tile -> position
+  std::vector<unsigned char> transposed;    // ... whether the permuted tile is its transpose
   Unpermute(const SplitCall& sc, int dev, cudaStream_t s) {
     const Pattern& C = sc.sel.closure;
     const Pattern& P = sc.so.permuted;
@@ -996,6 +1004,9 @@ struct Unpermute {
       vrs[static_cast<size_t>(i)] = sc.so.pos[static_cast<size_t>(i)];
     }
     count = static_cast<int>(C.size());
+    slot_of = vs;
+    transposed = vt;
+    pos = sc.so.pos;
     d = to_device(vd, dev, s);
     src = to_device(vs, dev, s);
     tr = to_device(vt, dev, s);
@@ -1005,9 +1016,16 @@ struct Unpermute {
   void run(const double* from, double* to, const double* var_from, double* var_to, int bp, cudaStream_t s) const {
     launch_permute_tiles(to, from, reinterpret_cast<const int*>(d.p), reinterpret_cast<const int*>(src.p),
                          reinterpret_cast<const unsigned char*>(tr.p), count, bp, 148 * 8, s);
-    launch_permute_rows(var_to, var_from, reinterpret_cast<const int*>(rd.p), reinterpret_cast<const int*>(rs.p), N,
-                        bp, s);
+    if (var_to)
+      launch_permute_rows(var_to, var_from, reinterpret_cast<const int*>(rd.p), reinterpret_cast<const int*>(rs.p), N,
+                          bp, s);
     CK(cudaGetLastError());
+  }
+  // offset of natural closure element (slot, r, c) in the permuted store
+  long long offset(long slot, int r, int c, int bp) const {
+    const long long k = slot_of[static_cast<size_t>(slot)];
+    return k * bp * bp + (transposed[static_cast<size_t>(slot)] ? static_cast<long long>(c) * bp + r
+                                                                 : static_cast<long long>(r) * bp + c);
   }
 };
 
@@ -1040,24 +1058,25 @@ static SigmaObj* selected_inverse_split(const MatrixObj& m, const Request& req, 
   nat->bp = bp;
   nat->nb = p2->nb;
   res->plan = nat;
-  res->S = DevBuf(sc.sel.closure.size() * bb, device, s);  // staging of transposed tiles, then Sigma
-  res->var = DevBuf(static_cast<size_t>(N) * bp, device, s);
-  DevBuf varp(static_cast<size_t>(N) * bp, device, s);
+  const bool stream_up = !m.gen.on && bp == m.layout.b && m.payload.pinned && streaming_allowed() &&
+                         fp->flow->host.upl >= 0;
+  // generator output / streamed columns land here before they are placed into A
+  DevBuf staging(m.gen.on || stream_up ? sc.sel.closure.size() * bb : 0, device, s);
+  res->var = DevBuf(static_cast<size_t>(N) * bp, device, s);  // permuted order
+  DevBuf& varp = res->var;
   tm.mark("allocations");
   // factor sweep on the permuted A store; phase 2 writes Sigma' over A (dead by then)
-  std::vector<BaseTable> tf{make_table(st.A.p, st.L.p, st.P1.p, res->S.p, varp.p, st.scratch.p, st.logdet.p,
+  std::vector<BaseTable> tf{make_table(st.A.p, st.L.p, st.P1.p, staging.p, varp.p, st.scratch.p, st.logdet.p,
                                        st.status.p, st.ctr(0))};
   std::vector<BaseTable> tp{make_table(st.A.p, st.L.p, st.P1.p, st.A.p, varp.p, st.scratch.p, st.logdet.p,
                                        st.status.p, st.ctr(0))};
-  const bool stream_up = !m.gen.on && bp == m.layout.b && m.payload.pinned && streaming_allowed() &&
-                         fp->flow->host.upl >= 0;
   if (m.gen.on) {
     // natural tiles from the device generator into the staging store, then permuted
-    device_generate(m, sc.natural.filled, bp, res->S.p, s);
+    device_generate(m, sc.natural.filled, bp, staging.p, s);
     std::vector<int> d(T);
     for (size_t k = 0; k < T; ++k) d[k] = static_cast<int>(k);
     DevBuf dd = to_device(d, device, s), ds = to_device(sc.src_filled, device, s), dt = to_device(sc.tr, device, s);
-    launch_permute_tiles(st.A.p, res->S.p, reinterpret_cast<const int*>(dd.p), reinterpret_cast<const int*>(ds.p),
+    launch_permute_tiles(st.A.p, staging.p, reinterpret_cast<const int*>(dd.p), reinterpret_cast<const int*>(ds.p),
                          reinterpret_cast<const unsigned char*>(dt.p), static_cast<int>(T), bp, 148 * 8, s);
     CK(cudaGetLastError());
     tm.mark("generate");
@@ -1148,7 +1167,7 @@ static SigmaObj* selected_inverse_split(const MatrixObj& m, const Request& req, 
           sent[static_cast<size_t>(nj)] = 1;
           const long k0 = Mp.col_start(nj), k1 = Mp.col_start(nj + 1);
           const long d = direct[static_cast<size_t>(nj)];
-          double* dst = d >= 0 ? st.A.p + static_cast<size_t>(d) * bb : res->S.p + static_cast<size_t>(k0) * bb;
+          double* dst = d >= 0 ? st.A.p + static_cast<size_t>(d) * bb : staging.p + static_cast<size_t>(k0) * bb;
           CK(cudaMemcpyAsync(dst, m.payload.p + static_cast<size_t>(k0) * bb, static_cast<size_t>(k1 - k0) * bb * sizeof(double),
                              cudaMemcpyHostToDevice, rt.upload));
         }
@@ -1165,8 +1184,9 @@ static SigmaObj* selected_inverse_split(const MatrixObj& m, const Request& req, 
   tm.mark("factor sweep");
   phase2_sweep(*p2, s, tp);
   tm.mark("phase-2 sweep");
-  Unpermute(sc, device, s).run(st.A.p, res->S.p, varp.p, res->var.p, bp, s);
-  tm.mark("unpermute");
+  staging.release();
+  res->unperm = std::make_shared<const Unpermute>(sc, device, s);
+  res->Sp = std::move(st.A);  // Sigma' (phase 2 wrote it over the A store)
   std::vector<double> parts(fp->flow->host.logdet_doubles);
   CK(cudaMemcpyAsync(parts.data(), st.logdet.p, parts.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
   check_status(st.status, 1, m.layout, s);  // a NotSpd here is re-run in the natural order by the caller
@@ -1318,11 +1338,24 @@ static void download_tiles(const DevBuf& store, const Pattern& pat, int b, int b
   }
 }
 
+// The natural-order Sigma store (un-permuted on first use after a two-chain call).
+static const DevBuf& sigma_store(SigmaObj& sg) {
+  if (sg.unperm && !sg.S.p) {
+    DeviceRt& rt = runtime(sg.device);
+    const int bp = sg.plan->bp;
+    sg.S = DevBuf(sg.plan->sel.closure.size() * static_cast<size_t>(bp) * bp, sg.device, rt.stream);
+    sg.unperm->run(sg.Sp.p, sg.S.p, nullptr, nullptr, bp, rt.stream);
+    CK(cudaStreamSynchronize(rt.stream));
+  }
+  return sg.S;
+}
+
 static const double* sigma_host(SigmaObj& sg) {
   if (!sg.host) {
     DeviceRt& rt = runtime(sg.device);
-    auto h = std::make_unique<HostBuf>(sg.S.n);
-    CK(cudaMemcpyAsync(h->p, sg.S.p, h->n * sizeof(double), cudaMemcpyDeviceToHost, rt.stream));
+    const DevBuf& S = sigma_store(sg);
+    auto h = std::make_unique<HostBuf>(S.n);
+    CK(cudaMemcpyAsync(h->p, S.p, h->n * sizeof(double), cudaMemcpyDeviceToHost, rt.stream));
     CK(cudaStreamSynchronize(rt.stream));
     sg.host = std::move(h);
   }
@@ -1902,7 +1935,12 @@ int tib_sigma_diagonal(tib_sigma sg, double* out) {
     std::vector<double> v(sg->var.n);
     CK(cudaMemcpyAsync(v.data(), sg->var.p, v.size() * sizeof(double), cudaMemcpyDeviceToHost, rt.stream));
     CK(cudaStreamSynchronize(rt.stream));
-    for (long r = 0; r < L.n; ++r) out[r] = v[static_cast<size_t>(r / L.b) * bp + static_cast<size_t>(r % L.b)];
+    // (two-chain order: tile row i of the variances is at position pos[i])
+    const std::vector<int>* pos = sg->unperm ? &sg->unperm->pos : nullptr;
+    for (long r = 0; r < L.n; ++r) {
+      const long i = r / L.b;
+      out[r] = v[static_cast<size_t>(pos ? (*pos)[static_cast<size_t>(i)] : i) * bp + static_cast<size_t>(r % L.b)];
+    }
   });
 }
 int tib_sigma_entries(tib_sigma sg, long* count, long* rows, long* cols, double* vals) {
@@ -1927,12 +1965,23 @@ int tib_sigma_entries(tib_sigma sg, long* count, long* rows, long* cols, double*
         if (cols) cols[k] = c;
         if (vals)
           at.push_back(static_cast<long long>(slot) * bp * bp + static_cast<long long>(a.row_off) * bp + a.col_off);
+        if (vals && sg->unperm && !sg->S.p) at.back() = sg->unperm->offset(slot, a.row_off, a.col_off, bp);
       }
       ++k;
     });
     *count = k;
     if (!vals || at.empty()) return;
-    if (sg->host || at.size() * 16 > sg->S.n) {  // (or already on the host)
+    const bool permuted = sg->unperm && !sg->S.p;  // offsets above are into Sp
+    const size_t store = permuted ? sg->Sp.n : sg->S.n;
+    if (sg->host || at.size() * 16 > store) {  // most of the store (or already on the host)
+      if (permuted) {  // natural offsets again, into the un-permuted host copy
+        long e = 0;
+        for_each_request_entry(L, C, sg->plan->sel.requested, sg->req, [&](long r, long c) {
+          const Address a = map_entry_to_tile(L, r, c);
+          at[static_cast<size_t>(e++)] = static_cast<long long>(C.slot(a.tile.i, a.tile.j)) * bp * bp +
+                                         static_cast<long long>(a.row_off) * bp + a.col_off;
+        });
+      }
       const double* h = sigma_host(*sg);
       for (size_t e = 0; e < at.size(); ++e) vals[e] = h[at[e]];
       return;
@@ -1940,7 +1989,8 @@ int tib_sigma_entries(tib_sigma sg, long* count, long* rows, long* cols, double*
     DeviceRt& rt = runtime(sg->device);
     DevBuf idx((at.size() + 0), sg->device, rt.stream), out(at.size(), sg->device, rt.stream);
     CK(cudaMemcpyAsync(idx.p, at.data(), at.size() * sizeof(long long), cudaMemcpyHostToDevice, rt.stream));
-    launch_gather(sg->S.p, reinterpret_cast<const long long*>(idx.p), out.p, static_cast<long long>(at.size()), rt.stream);
+    launch_gather(permuted ? sg->Sp.p : sg->S.p, reinterpret_cast<const long long*>(idx.p), out.p,
+                  static_cast<long long>(at.size()), rt.stream);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(vals, out.p, at.size() * sizeof(double), cudaMemcpyDeviceToHost, rt.stream));
     CK(cudaStreamSynchronize(rt.stream));
@@ -1950,7 +2000,7 @@ int tib_sigma_tiles(tib_sigma sg, int* ti, int* tj, double* payload) {
   return guarded([&] {
     need(sg, "result");
     DeviceRt& rt = runtime(sg->device);
-    download_tiles(sg->S, sg->plan->sel.closure, sg->layout.b, sg->plan->bp, ti, tj, payload, rt.stream, false);
+    download_tiles(sigma_store(*sg), sg->plan->sel.closure, sg->layout.b, sg->plan->bp, ti, tj, payload, rt.stream, false);
   });
 }
 int tib_sigma_checksum(tib_sigma sg, uint64_t* out) {
@@ -1967,7 +2017,7 @@ int tib_sigma_write_stls(tib_sigma sg, const char* path) {
     const Pattern& C = sg->plan->sel.closure;
     const size_t bb = static_cast<size_t>(sg->layout.b) * sg->layout.b;
     std::vector<double> pay(C.size() * bb);
-    download_tiles(sg->S, C, sg->layout.b, sg->plan->bp, nullptr, nullptr, pay.data(), rt.stream, false);
+    download_tiles(sigma_store(*sg), C, sg->layout.b, sg->plan->bp, nullptr, nullptr, pay.data(), rt.stream, false);
     write_tile_file(path, sg->layout, 3, C, pay.data());
   });
 }
@@ -2213,11 +2263,9 @@ struct tib_resident_s {
   std::vector<BaseTable> tables;
   double logdet = 0;
   double model_flops = 0;
-  // two-chain order (one matrix): the stores hold the permuted matrix, and
-  // each run ends with Sigma / the variances un-permuted into Sn / varn
+  // two-chain order (one matrix): the stores hold the permuted matrix (like a
+  // public call's result, Sigma stays in that order until an accessor needs it)
   std::unique_ptr<SplitCall> split;
-  std::unique_ptr<Unpermute> unperm;
-  DevBuf Sn, varn;
 };
 
 extern "C" {
@@ -2275,11 +2323,7 @@ int tib_resident_create_batch(const tib_matrix* ms, int count, int device, tib_r
     }
     r->Sg = DevBuf(C * tile * count, device, s);
     r->var = DevBuf(nv * count, device, s);
-    if (so) {
-      r->unperm = std::make_unique<Unpermute>(*r->split, device, s);
-      r->Sn = DevBuf(C * tile, device, s);
-      r->varn = DevBuf(nv, device, s);
-    }
+
     for (int k = 0; k < count; ++k)
       r->tables.push_back(make_table(r->st.A.p + T * tile * k, r->st.L.p + T * tile * k, r->st.P1.p + T * tile * k,
                                      r->Sg.p + C * tile * k, r->var.p + nv * k,
@@ -2305,7 +2349,6 @@ int tib_resident_run(tib_resident r, int reps, double* ms_total, double* ms_fact
       factor_sweep(*r->fp, r->st, s, r->tables);
       CK(cudaEventRecord(ev[3 * it + 1], s));
       phase2_sweep(*r->p2, s, r->tables);
-      if (r->unperm) r->unperm->run(r->Sg.p, r->Sn.p, r->var.p, r->varn.p, r->fp->bp, s);
       CK(cudaEventRecord(ev[3 * it + 2], s));
     }
     CK(cudaEventSynchronize(ev.back()));
