@@ -348,11 +348,36 @@ static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int 
   return plan;
 }
 
+// Late terms per phase-2 split-K part.  Batches, and the two-chain order with
+// large tiles (>= 8 blocks), run a throughput-bound phase 2, where fewer,
+// larger parts win (two-chain large 101.3 -> 99.8 ms, batch 137 -> 128 ms at
+// 3); a single chain is latency-bound there (natural-order large 101.8 ->
+// 117.5 ms, two-chain medium 17 -> 27 ms at 3), so one term per part.
+// Update work per elimination step relative to the chain: (tiles per column)^2
+// x (blocks per tile)^2.  Above TIB_SPLIT_WORK the sweeps are throughput bound
+// even with one chain (Kronecker), below it a single chain bounds them.
+static double chain_work(const Pattern& F) {
+  const int N = F.layout().N;
+  const double per_col = static_cast<double>(F.size() - static_cast<size_t>(N)) / N;
+  const double nbk = static_cast<double>((F.layout().b + 63) / 64);
+  return per_col * per_col * nbk * nbk;
+}
+
+static int phase2_group(const Pattern& F, int batch, int split) {
+  const int forced = env_int("TIB_P2_GROUP", 0);
+  if (forced > 0) return forced;
+  const int nb = (F.layout().b + 63) / 64;
+  const bool throughput = batch > 4 || (split > 0 && nb >= 8) || chain_work(F) > env_int("TIB_SPLIT_WORK", 3000);
+  return throughput ? 3 : 1;
+}
+
 static std::shared_ptr<Phase2Plan> phase2_plan_for(const Pattern& F, const Closure& sel, int device,
-                                                   cudaStream_t s, int crit = -1, int split = -1) {
+                                                   cudaStream_t s, int crit = -1, int split = -1, int batch = 1) {
   if (crit < 0) crit = crit_workers(false);
+  const int group = phase2_group(F, batch, split);
   const uint64_t key = pattern_hash(
-      sel.closure, pattern_hash(F, 2 + 7919ull * static_cast<uint64_t>(crit) + 104729ull * static_cast<uint64_t>(split + 2)));
+      sel.closure, pattern_hash(F, 2 + 7919ull * static_cast<uint64_t>(crit) + 104729ull * static_cast<uint64_t>(split + 2) +
+                                       1299709ull * static_cast<uint64_t>(group)));
   {
     std::lock_guard<std::mutex> lk(g_plan_mu);
     auto it = g_p2plans.find({device, key});
@@ -360,7 +385,7 @@ static std::shared_ptr<Phase2Plan> phase2_plan_for(const Pattern& F, const Closu
   }
   auto plan = std::make_shared<Phase2Plan>();
   plan->sel = sel;
-  plan->flow = upload_plan(build_phase2_dataflow(F, plan->sel, crit, split), device, s);
+  plan->flow = upload_plan(build_phase2_dataflow(F, plan->sel, crit, split, group), device, s);
   plan->flow->crit_batch = crit_workers_batch(false);
   plan->flow->c0_prefetch = env_int("TIB_C0_PF_P2", 1);
   plan->bp = plan->flow->host.bp;
@@ -947,11 +972,8 @@ static bool split_call(const MatrixObj& m, const Request& req, SplitCall& sc) {
   if (env_int("TIB_SPLIT", 1) == 0) return false;
   sc.natural = symbolic_cholesky(m.pattern);
   const Pattern& F = sc.natural.filled;
-  // chain-bound sweeps only: the update work per chain step grows with the
-  // square of the tiles per column and of the blocks per tile
-  const double per_col = static_cast<double>(F.size() - static_cast<size_t>(F.layout().N)) / F.layout().N;
-  const double nbk = static_cast<double>((F.layout().b + 63) / 64);
-  if (per_col * per_col * nbk * nbk > env_int("TIB_SPLIT_WORK", 3000)) return false;
+  // chain-bound sweeps only
+  if (chain_work(F) > env_int("TIB_SPLIT_WORK", 3000)) return false;
   sc.sel = symbolic_inversion(select_tiles(F.layout(), F, req), F);
   if (!(sc.sel.closure == F)) return false;  // Sigma on the whole factor pattern only
   sc.so = two_chain_order(F);
@@ -2041,7 +2063,7 @@ int tib_selected_inverse_batch(const tib_matrix* ms, int count, int device, doub
     Request req;
     req.preset = kFactorPattern;
     const Closure sel = symbolic_inversion(select_tiles(F.layout(), F, req), F);
-    auto p2 = phase2_plan_for(F, sel, device, s);
+    auto p2 = phase2_plan_for(F, sel, device, s, -1, -1, count);
     tm.mark("plans");
     const size_t tile = static_cast<size_t>(fp->bp) * fp->bp;
     SweepStores st;
@@ -2229,7 +2251,7 @@ int tib_plan_export(tib_matrix m, int preset, const long* rows, const long* cols
     } else {
       const Closure sel =
           symbolic_inversion(select_tiles(sym.filled.layout(), sym.filled, make_request(preset, rows, cols, ne)), sym.filled);
-      P = build_phase2_dataflow(sym.filled, sel, crit_workers, split);
+      P = build_phase2_dataflow(sym.filled, sel, crit_workers, split, phase2_group(sym.filled, 1, split));
     }
     if (sizes) {
       sizes[0] = static_cast<double>(P.tasks.size());
@@ -2301,7 +2323,7 @@ int tib_resident_create_batch(const tib_matrix* ms, int count, int device, tib_r
     const Pattern& F = r->fp->sym.filled;
     const Closure sel = symbolic_inversion(select_tiles(F.layout(), F, req), F);
     r->p2 = so ? phase2_plan_for(F, sel, device, s, env_int("TIB_CRIT_SPLIT_P2", 24), so->split)
-               : phase2_plan_for(F, sel, device, s);
+               : phase2_plan_for(F, sel, device, s, -1, -1, count);
     // the reference's task model counts the reference's own (natural) order
     const Closure sel_nat = symbolic_inversion(select_tiles(natural.filled.layout(), natural.filled, req), natural.filled);
     const Flops fl = count_flops(natural, &sel_nat);

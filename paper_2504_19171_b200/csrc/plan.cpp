@@ -871,7 +871,7 @@ DataflowPlan build_phase1_dataflow(const Pattern& F) {
   return P;
 }
 
-DataflowPlan build_phase2_dataflow(const Pattern& F, const Closure& sel, int crit_workers, int split) {
+DataflowPlan build_phase2_dataflow(const Pattern& F, const Closure& sel, int crit_workers, int split, int group) {
   DataflowPlan P;
   P.L = F.layout();
   const int bp = (P.L.b + kB - 1) / kB * kB, nb = bp / kB, NB2 = nb * nb;
@@ -886,6 +886,9 @@ DataflowPlan build_phase2_dataflow(const Pattern& F, const Closure& sel, int cri
   // frees the ring slot (implied by the data dependencies on band patterns,
   // enforced for any other closure).
   constexpr int kRing = 4;
+  // late terms are split-K parts of `group` terms each (K = 512 * group at b = 512)
+  const int G = std::max(1, group);
+  auto groups = [&](int terms) { return (terms + G - 1) / G; };
   std::vector<int> col_slots(static_cast<size_t>(N), 0);
   std::vector<std::vector<int>> Kof(static_cast<size_t>(N));
   for (const ColumnWork& cw : sel.columns) {
@@ -899,9 +902,10 @@ DataflowPlan build_phase2_dataflow(const Pattern& F, const Closure& sel, int cri
     for (int j : cw.offdiag_rows) {
       int late = 0;
       for (int k : K) late += std::min(j, k) == kc ? 1 : 0;
-      if (late > 1) n += NB2 * late;
+      const int g = groups(late);
+      if (g > 1) n += NB2 * g;
     }
-    if (cw.diagonal) n += nb * (nb + 1) / 2 * (1 + static_cast<int>(K.size()));
+    if (cw.diagonal) n += nb * (nb + 1) / 2 * (1 + groups(static_cast<int>(K.size())));
     col_slots[static_cast<size_t>(i)] = n;
   }
   const int slots_per_col = *std::max_element(col_slots.begin(), col_slots.end());
@@ -974,7 +978,7 @@ DataflowPlan build_phase2_dataflow(const Pattern& F, const Closure& sel, int cri
       const long ts = cslot(j, i);
       std::vector<int> early, late;
       for (int k : K) (std::min(j, k) == kcrit ? late : early).push_back(k);
-      const int parts = static_cast<int>(late.size());
+      const int parts = groups(static_cast<int>(late.size()));
       for (int p = 0; p < nb; ++p)
         for (int q = 0; q < nb; ++q) {
           if (!early.empty()) {
@@ -993,7 +997,12 @@ DataflowPlan build_phase2_dataflow(const Pattern& F, const Closure& sel, int cri
           }
           const int base = slot_next;
           for (int r = 0; r < parts; ++r) {
-            std::vector<Dep> d{mdep(j, late[static_cast<size_t>(r)])};
+            const size_t g0 = static_cast<size_t>(r) * G, g1 = std::min(late.size(), g0 + G);
+            std::vector<Dep> d;
+            for (size_t x = g0; x < g1; ++x) d.push_back(mdep(j, late[x]));
+            std::sort(d.begin(), d.end(), [](const Dep& x, const Dep& y) { return x.counter < y.counter; });
+            d.erase(std::unique(d.begin(), d.end(), [](const Dep& x, const Dep& y) { return x.counter == y.counter; }),
+                    d.end());
             std::vector<Dep> d2;
             if (!early.empty()) d2.push_back({spart(ts, p, q), 1});
             if (parts > 1) d.insert(d.end(), ring_deps.begin(), ring_deps.end());
@@ -1009,7 +1018,7 @@ DataflowPlan build_phase2_dataflow(const Pattern& F, const Closure& sel, int cri
             t.m0 = p * kB;
             t.n0 = q * kB;
             if (parts > 1) take(parts, t, r, base);
-            mseg(t, j, late[static_cast<size_t>(r)]);
+            for (size_t x = g0; x < g1; ++x) mseg(t, j, late[x]);
           }
           if (parts > 1) slot_next += parts;
         }
@@ -1020,18 +1029,18 @@ DataflowPlan build_phase2_dataflow(const Pattern& F, const Closure& sel, int cri
     if (cw.diagonal) {
       const long dsl = cslot(i, i);
       const long xs = F.col_start(i);
-      const int parts = 1 + static_cast<int>(K.size());
+      const int parts = 1 + groups(static_cast<int>(K.size()));
       for (int p = 0; p < nb; ++p)
         for (int q = 0; q <= p; ++q) {
           const int base = slot_next;
           for (int r = 0; r < parts; ++r) {
             std::vector<Dep> d;
+            const size_t g0 = r == 0 ? 0 : static_cast<size_t>(r - 1) * G, g1 = r == 0 ? 0 : std::min(K.size(), g0 + G);
             if (r == 0) {
               // the LAUUM part runs when the column becomes active
               if (kcrit >= 0 && C.slot(kcrit, kcrit) >= 0) d.push_back(mdep(kcrit, kcrit));
             } else {
-              const long ks = cslot(K[static_cast<size_t>(r - 1)], i);
-              d.push_back({sfin(ks), NB2});
+              for (size_t x = g0; x < g1; ++x) d.push_back({sfin(cslot(K[x], i)), NB2});
             }
             if (parts > 1) d.insert(d.end(), ring_deps.begin(), ring_deps.end());
             DTask& t = B.add(0, d, {sfin(dsl)});
@@ -1054,9 +1063,11 @@ DataflowPlan build_phase2_dataflow(const Pattern& F, const Closure& sel, int cri
               // U U^T = X^T X; rows >= p*64 of X carry the nonzeros for block row p >= q
               B.seg(t, kStoreP1, tile_off(xs, bp), kStoreP1, tile_off(xs, bp), p * kB, bp, kTransA);
             } else {
-              const int k = K[static_cast<size_t>(r - 1)];
-              B.seg(t, kStoreP1, tile_off(F.slot(k, i), bp), kStoreSigma, tile_off(cslot(k, i), bp), 0, bp,
-                    kTransA | kNegate);
+              for (size_t x = g0; x < g1; ++x) {
+                const int k = K[x];
+                B.seg(t, kStoreP1, tile_off(F.slot(k, i), bp), kStoreSigma, tile_off(cslot(k, i), bp), 0, bp,
+                      kTransA | kNegate);
+              }
             }
           }
           if (parts > 1) slot_next += parts;

@@ -75,7 +75,9 @@ DataflowPlan build_phase1_dataflow(const Pattern& filled);
 // terms and the first-row term; the first-row chain is queue 0.
 // split > 0 (two-chain order): the columns below split get their own ring of
 // split-K slots (an independent chain once the columns above are done).
-DataflowPlan build_phase2_dataflow(const Pattern& filled, const Closure& sel, int crit_workers, int split = -1);
+// group: late (critical) terms per split-K part.
+DataflowPlan build_phase2_dataflow(const Pattern& filled, const Closure& sel, int crit_workers, int split = -1,
+                                   int group = 1);
 
 // Simulates the plan in its global emission order (queue 0 and queue 1 are
 // both subsequences of it) and throws ConsistencyError if any dependency is

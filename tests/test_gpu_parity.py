@@ -144,6 +144,7 @@ def test_factor_path_and_determinism(tib, orc, monkeypatch):
 # 80 > the reserved critical workers: every chain still runs on its own worker
 def test_batch_matches_single(tib, count, monkeypatch):
     monkeypatch.setenv("TIB_SPLIT", "0")  # single calls in the batch's (natural) elimination order
+    monkeypatch.setenv("TIB_P2_GROUP", "1")  # ... and its phase-2 term grouping
     b = 256 if count > 6 else 128
     ms = [tib.generate(5000, 500, 50, 1.0, seed=1000 + k, tile_size=b) for k in range(count)]
     logdet, diag = tib.selected_inverse_batch(ms)
@@ -275,10 +276,12 @@ def test_arrow_only_vs_oracle(tib, orc, case):
     assert abs(res.logdet() - ref["logdet"]) <= TOL * abs(ref["logdet"])
 
 
-def test_batch_larger_than_one_launch(tib):
+def test_batch_larger_than_one_launch(tib, monkeypatch):
     """More matrices than CTAs (static chain assignment) and more than the
     old 7-bit item packing allowed: the engine runs the batch in launches of
     at most one chain per CTA."""
+    monkeypatch.setenv("TIB_SPLIT", "0")  # single calls in the batch's order and grouping
+    monkeypatch.setenv("TIB_P2_GROUP", "1")
     ms = [tib.generate(300, 40, 7, 1.0, seed=500 + k, tile_size=64) for k in range(300)]
     logdet, diag = tib.selected_inverse_batch(ms)
     for k in (0, 127, 128, 147, 148, 299):
