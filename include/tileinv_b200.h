@@ -196,12 +196,14 @@ int tib_selected_inverse_batch(const tib_matrix* ms, int count, int device, doub
 /* ---- dataflow plans (host only; inspection and CPU-side simulation) -------- */
 /* Builds the device task plan of one sweep (which = 0: fused factorization +
  * phase 1, which = 1: phase 2 for the request) WITHOUT a GPU and copies it
- * out.  sizes[0..9] = {tasks, queue-0 tasks, segments, deps, signals,
+ * out, as the engine builds it for a launch of `batch` matrices (split > 0:
+ * the two-chain order's plan).  sizes[0..9] = {tasks, queue-0 tasks, segments, deps, signals,
  * counters, bp, scratch doubles, executed FLOPs, sizeof(DTask)}; call with
  * NULL buffers to query.  Layouts are the POD structs of taskfmt.hpp.        */
 typedef struct tib_resident_s* tib_resident;
 int tib_plan_export(tib_matrix m, int preset, const long* rows, const long* cols, long nentries, int which,
-                    int crit_workers, int split, double* sizes, void* tasks, void* segs, void* deps, void* sigs);
+                    int crit_workers, int split, int batch, double* sizes, void* tasks, void* segs, void* deps,
+                    void* sigs);
 /* Two-chain elimination order of a single-matrix call: for a
  * band + arrow tile pattern, order[k] (N entries, may be NULL) = the original
  * tile at position k of [I_0 ascending, I_1 descending, separator, arrow];

@@ -632,15 +632,16 @@ def two_chain_permuted(matrix: Matrix) -> Matrix:
     return Matrix(h.value)
 
 
-def plan_export(matrix: Matrix, selection="pattern", which: int = 0, crit_workers: int = 16, split: int = -1) -> dict:
+def plan_export(matrix: Matrix, selection="pattern", which: int = 0, crit_workers: int = 16, split: int = -1,
+                batch: int = 1) -> dict:
     """Host-built dataflow plan of one device sweep (0: factorization + phase 1,
     1: phase 2 for `selection`) as numpy arrays; no GPU needed.  split > 0: the
     factor plan with a second elimination chain from that column on."""
     preset, rows, cols, ne = _request(selection)
     sizes = np.zeros(10, np.float64)
     dptr = sizes.ctypes.data_as(C.POINTER(C.c_double))
-    _check(lib.tib_plan_export(matrix._h, preset, _lp(rows), _lp(cols), ne, which, crit_workers, split, dptr,
-                               None, None, None, None))
+    _check(lib.tib_plan_export(matrix._h, preset, _lp(rows), _lp(cols), ne, which, crit_workers, split, batch,
+                               dptr, None, None, None, None))
     nt, nq0, ns, nd, nsig, ncnt, bp, scratch, flops, tsz = sizes.tolist()
     if int(tsz) != DTASK_DTYPE.itemsize:
         raise TileinvError(f"DTask layout mismatch: {int(tsz)} vs {DTASK_DTYPE.itemsize}")
@@ -648,8 +649,8 @@ def plan_export(matrix: Matrix, selection="pattern", which: int = 0, crit_worker
     segs = np.zeros(int(ns), SEG_DTYPE)
     deps = np.zeros(int(nd), DEP_DTYPE)
     sigs = np.zeros(int(nsig), np.int32)
-    _check(lib.tib_plan_export(matrix._h, preset, _lp(rows), _lp(cols), ne, which, crit_workers, split, dptr,
-                               tasks.ctypes.data_as(C.c_void_p), segs.ctypes.data_as(C.c_void_p),
+    _check(lib.tib_plan_export(matrix._h, preset, _lp(rows), _lp(cols), ne, which, crit_workers, split, batch,
+                               dptr, tasks.ctypes.data_as(C.c_void_p), segs.ctypes.data_as(C.c_void_p),
                                deps.ctypes.data_as(C.c_void_p), sigs.ctypes.data_as(C.c_void_p)))
     return {"tasks": tasks, "segs": segs, "deps": deps, "sigs": sigs, "q0": int(nq0), "counters": int(ncnt),
             "bp": int(bp), "scratch_doubles": int(scratch), "executed_flops": flops}

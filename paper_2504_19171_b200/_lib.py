@@ -80,7 +80,7 @@ SIGNATURES = {
     "tib_sigma_free": [_p],
     "tib_selected_inverse_batch": [_pp, _i, _i, _pd, _pd],
     "tib_bench_resident": [_p, _i, _i, _i, _pd, _pd, _pd, _pd],
-    "tib_plan_export": [_p, _i, _pl, _pl, _l, _i, _i, _i, _pd, _p, _p, _p, _p],
+    "tib_plan_export": [_p, _i, _pl, _pl, _l, _i, _i, _i, _i, _pd, _p, _p, _p, _p],
     "tib_matrix_two_chain_order": [_p, _pi, _pi],
     "tib_matrix_two_chain_permuted": [_p, _pp],
     "tib_resident_create": [_p, _i, _pp],

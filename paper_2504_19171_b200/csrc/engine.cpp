@@ -278,7 +278,7 @@ static int crit_workers(bool factor) {
   return factor ? env_int("TIB_CRIT_WORKERS_FACTOR", 56) : env_int("TIB_CRIT_WORKERS_P2", 12);
 }
 static int crit_workers_batch(bool factor) {
-  return factor ? env_int("TIB_CRIT_BATCH_FACTOR", 8) : env_int("TIB_CRIT_BATCH_P2", 40);
+  return factor ? env_int("TIB_CRIT_BATCH_FACTOR", 32) : env_int("TIB_CRIT_BATCH_P2", 40);
 }
 
 static std::shared_ptr<DevPlan> upload_plan(DataflowPlan&& host, int device, cudaStream_t s) {
@@ -320,9 +320,18 @@ static std::mutex g_plan_mu;
 static std::map<std::pair<int, uint64_t>, std::shared_ptr<FactorPlan2>> g_fplans;
 static std::map<std::pair<int, uint64_t>, std::shared_ptr<Phase2Plan>> g_p2plans;
 
+// batch > 4 (chains share their SMs): no chain task.  A batch is throughput
+// bound; a chain task would tie one worker per matrix for the whole sweep
+// (64 x 157 ms at config 5, ~11 % of it computing) and its fat steps wait in
+// the second phase for a backlogged bulk queue.  Plain leaves (no fat part,
+// no boundary trick) are ordinary tasks that never wait inside.
+static bool batch_leaves(int batch) { return batch > 4 && env_int("TIB_BATCH_CHAIN", 0) == 0; }
+
 static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int device, cudaStream_t s,
-                                                    int split = -1) {
-  const uint64_t key = pattern_hash(pattern, 1 + 0x9e3779b97f4a7c15ull * static_cast<uint64_t>(split + 2));
+                                                    int split = -1, int batch = 1) {
+  const bool leaves = batch_leaves(batch);
+  const uint64_t key = pattern_hash(pattern, 1 + 0x9e3779b97f4a7c15ull * static_cast<uint64_t>(split + 2) +
+                                                 (leaves ? 0x51ed27ull : 0));
   {
     std::lock_guard<std::mutex> lk(g_plan_mu);
     auto it = g_fplans.find({device, key});
@@ -333,10 +342,10 @@ static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int 
   plan->L = plan->sym.filled.layout();
   // two chains keep the critical queue busier per reserved worker (tools/ab_env.py: 24 / 24 best)
   const int crit = split > 0 ? env_int("TIB_CRIT_SPLIT_FACTOR", 24) : crit_workers(true);
-  // the device sweep: chain task, fat leaves and the tile-boundary trick
-  // always (the combinations the executor is tested with)
-  plan->flow = upload_plan(build_factor_dataflow(plan->sym.filled, crit, kDeferW, true, true, true,
-                                                  split),
+  // the device sweep: chain task, fat leaves and the tile-boundary trick, or
+  // (batches) plain leaf tasks -- the two configurations the executor is tested with
+  plan->flow = upload_plan(leaves ? build_factor_dataflow(plan->sym.filled, crit, kDeferW, false, false, false, split)
+                                  : build_factor_dataflow(plan->sym.filled, crit, kDeferW, true, true, true, split),
                            device, s);
   plan->flow->crit_batch = crit_workers_batch(true);
   plan->flow->c0_prefetch = env_int("TIB_C0_PF_FACTOR", 1);
@@ -2058,7 +2067,7 @@ int tib_selected_inverse_batch(const tib_matrix* ms, int count, int device, doub
     DeviceRt& rt = runtime(device);
     cudaStream_t s = rt.stream;
     HostTimer tm(s);
-    auto fp = factor_plan_for(m0.pattern, device, s);
+    auto fp = factor_plan_for(m0.pattern, device, s, -1, count);
     const Pattern& F = fp->sym.filled;
     Request req;
     req.preset = kFactorPattern;
@@ -2237,7 +2246,8 @@ int tib_matrix_two_chain_permuted(tib_matrix m, tib_matrix* out) {
 }
 
 int tib_plan_export(tib_matrix m, int preset, const long* rows, const long* cols, long ne, int which,
-                    int crit_workers, int split, double* sizes, void* tasks, void* segs, void* deps, void* sigs) {
+                    int crit_workers, int split, int batch, double* sizes, void* tasks, void* segs, void* deps,
+                    void* sigs) {
   return guarded([&] {
     need(m, "matrix");
     if (which != 0 && which != 1) throw Error(kErrInvalidArgument, "which must be 0 (factor) or 1 (phase 2)");
@@ -2247,11 +2257,12 @@ int tib_plan_export(tib_matrix m, int preset, const long* rows, const long* cols
     if (which == 0) {
       // the CPU simulator runs the same decomposition as the GPU chain, with the
       // chain's steps kept as (fat / boundary) leaf tasks
-      P = build_factor_dataflow(sym.filled, crit_workers, kDeferW, true, false, true, split);
+      P = batch_leaves(batch) ? build_factor_dataflow(sym.filled, crit_workers, kDeferW, false, false, false, split)
+                              : build_factor_dataflow(sym.filled, crit_workers, kDeferW, true, false, true, split);
     } else {
       const Closure sel =
           symbolic_inversion(select_tiles(sym.filled.layout(), sym.filled, make_request(preset, rows, cols, ne)), sym.filled);
-      P = build_phase2_dataflow(sym.filled, sel, crit_workers, split, phase2_group(sym.filled, 1, split));
+      P = build_phase2_dataflow(sym.filled, sel, crit_workers, split, phase2_group(sym.filled, batch, split));
     }
     if (sizes) {
       sizes[0] = static_cast<double>(P.tasks.size());
@@ -2319,7 +2330,7 @@ int tib_resident_create_batch(const tib_matrix* ms, int count, int device, tib_r
       if (count == 1 && split_call(*m, req, *sc)) r->split = std::move(sc);
     }
     const SplitOrder* so = r->split ? &r->split->so : nullptr;
-    r->fp = so ? factor_plan_for(so->permuted, device, s, so->split) : factor_plan_for(m->pattern, device, s);
+    r->fp = so ? factor_plan_for(so->permuted, device, s, so->split) : factor_plan_for(m->pattern, device, s, -1, count);
     const Pattern& F = r->fp->sym.filled;
     const Closure sel = symbolic_inversion(select_tiles(F.layout(), F, req), F);
     r->p2 = so ? phase2_plan_for(F, sel, device, s, env_int("TIB_CRIT_SPLIT_P2", 24), so->split)

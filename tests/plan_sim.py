@@ -184,15 +184,15 @@ class Sim:
             raise RuntimeError(f"dataflow deadlock: {done} of {len(tasks)} tasks ran")
 
 
-def run_plans(tib, matrix, selection, order=None, split=-1):
+def run_plans(tib, matrix, selection, order=None, split=-1, batch=1):
     """Runs factor + phase-2 plans of `matrix` on the CPU interpreter (in-order
     queue claiming, or a random ready order seeded by `order`; split > 0: the
     two-chain factor plan); returns (factor tiles, closure tiles, Sigma payload
     [T, b, b], logdet, first bad pivot)."""
     fpat = tib.factor_pattern(matrix)
     closure, _ = tib.closure_tiles(matrix, selection)
-    pf = tib.plan_export(matrix, selection, 0, crit_workers=1, split=split)
-    pp = tib.plan_export(matrix, selection, 1, crit_workers=1, split=split)
+    pf = tib.plan_export(matrix, selection, 0, crit_workers=1, split=split, batch=batch)
+    pp = tib.plan_export(matrix, selection, 1, crit_workers=1, split=split, batch=batch)
     bp, b, n = pf["bp"], matrix.tile_size, matrix.n
     N = matrix.n_tiles
     nb = bp // BLK

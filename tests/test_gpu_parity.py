@@ -143,10 +143,19 @@ def test_factor_path_and_determinism(tib, orc, monkeypatch):
 @pytest.mark.parametrize("count", [3, 6, 80])  # 6 > TIB_DEDICATE_MAX_BATCH: chains share their SMs;
 # 80 > the reserved critical workers: every chain still runs on its own worker
 def test_batch_matches_single(tib, count, monkeypatch):
-    monkeypatch.setenv("TIB_SPLIT", "0")  # single calls in the batch's (natural) elimination order
-    monkeypatch.setenv("TIB_P2_GROUP", "1")  # ... and its phase-2 term grouping
     b = 256 if count > 6 else 128
     ms = [tib.generate(5000, 500, 50, 1.0, seed=1000 + k, tile_size=b) for k in range(count)]
+    # a batch of more than 4 runs plain leaf tasks and groups phase 2's late
+    # terms: the same values to rounding
+    logdet, diag = tib.selected_inverse_batch(ms)
+    monkeypatch.setenv("TIB_SPLIT", "0")  # single calls in the batch's (natural) elimination order
+    for k in (0, count - 1):
+        res = tib.selected_inverse(ms[k], "pattern")
+        assert abs(logdet[k] - res.logdet()) <= 1e-13 * abs(res.logdet())
+        assert elementwise(diag[k], res.diagonal()) <= 1e-12
+    # with the single call's task structure, the same bits
+    monkeypatch.setenv("TIB_BATCH_CHAIN", "1")
+    monkeypatch.setenv("TIB_P2_GROUP", "1")
     logdet, diag = tib.selected_inverse_batch(ms)
     for k in (range(count) if count <= 6 else (0, 1, count - 2, count - 1)):
         res = tib.selected_inverse(ms[k], "pattern")
@@ -280,8 +289,9 @@ def test_batch_larger_than_one_launch(tib, monkeypatch):
     """More matrices than CTAs (static chain assignment) and more than the
     old 7-bit item packing allowed: the engine runs the batch in launches of
     at most one chain per CTA."""
-    monkeypatch.setenv("TIB_SPLIT", "0")  # single calls in the batch's order and grouping
+    monkeypatch.setenv("TIB_SPLIT", "0")  # single calls in the batch's order, tasks and grouping
     monkeypatch.setenv("TIB_P2_GROUP", "1")
+    monkeypatch.setenv("TIB_BATCH_CHAIN", "1")
     ms = [tib.generate(300, 40, 7, 1.0, seed=500 + k, tile_size=64) for k in range(300)]
     logdet, diag = tib.selected_inverse_batch(ms)
     for k in (0, 127, 128, 147, 148, 299):

@@ -143,3 +143,19 @@ def test_plan_simulation_two_chains(tib, orc, case, order):
         rows = min(b, n - perm[k] * b)
         back[perm[k] * b: perm[k] * b + rows] = var[k * b: k * b + rows]
     assert normwise(back, nat["diag"]) <= 1e-12
+
+
+@pytest.mark.parametrize("case", CASES[:3] + CASES[5:], ids=[str(c[:6]) for c in CASES[:3] + CASES[5:]])
+@pytest.mark.parametrize("order", [None, 3])
+def test_plan_simulation_batch_plans(tib, orc, case, order):
+    """The plans of a batched launch (more than 4 matrices): plain leaf tasks
+    instead of the chain task, phase-2 late terms three to a part."""
+    n, w, t, d, seed, b, sel = case
+    if sel != "pattern":
+        return
+    m = tib.generate(n, w, t, d, seed=seed, tile_size=b)
+    fpat, closure, sig, logdet, bad, var = run_plans(tib, m, sel, order=order, batch=64)
+    ref = orc.selected_inverse_generated(n, w, t, d, seed, b, sel)
+    assert closure == ref["tiles"]
+    assert normwise(sig, ref["payload"]) <= 1e-12
+    assert abs(logdet - ref["logdet"]) <= 1e-12 * abs(ref["logdet"])
