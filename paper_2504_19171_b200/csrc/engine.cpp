@@ -325,7 +325,12 @@ static std::map<std::pair<int, uint64_t>, std::shared_ptr<Phase2Plan>> g_p2plans
 // (64 x 157 ms at config 5, ~11 % of it computing) and its fat steps wait in
 // the second phase for a backlogged bulk queue.  Plain leaves (no fat part,
 // no boundary trick) are ordinary tasks that never wait inside.
-static bool batch_leaves(int batch) { return batch > 4 && env_int("TIB_BATCH_CHAIN", 0) == 0; }
+// Only launches of many matrices: with fewer in flight (the host batch's
+// pipelined groups of 16) each matrix's chain of leaf tasks, every step a trip
+// through the queues, becomes the bound (groups of 16: 447 -> 475 ms e2e).
+static bool batch_leaves(int batch) {
+  return batch >= env_int("TIB_BATCH_LEAVES_MIN", 32) && env_int("TIB_BATCH_CHAIN", 0) == 0;
+}
 
 static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int device, cudaStream_t s,
                                                     int split = -1, int batch = 1) {
@@ -347,7 +352,9 @@ static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int 
   plan->flow = upload_plan(leaves ? build_factor_dataflow(plan->sym.filled, crit, kDeferW, false, false, false, split)
                                   : build_factor_dataflow(plan->sym.filled, crit, kDeferW, true, true, true, split),
                            device, s);
-  plan->flow->crit_batch = crit_workers_batch(true);
+  // reserved critical workers of launches without dedicated chain SMs: more
+  // for leaf tasks (the whole chain goes through the critical queue)
+  plan->flow->crit_batch = leaves ? crit_workers_batch(true) : env_int("TIB_CRIT_BATCH_CHAINS", 8);
   plan->flow->c0_prefetch = env_int("TIB_C0_PF_FACTOR", 1);
   plan->bp = plan->flow->host.bp;
   plan->nb = plan->flow->host.nb;
@@ -2067,7 +2074,12 @@ int tib_selected_inverse_batch(const tib_matrix* ms, int count, int device, doub
     DeviceRt& rt = runtime(device);
     cudaStream_t s = rt.stream;
     HostTimer tm(s);
-    auto fp = factor_plan_for(m0.pattern, device, s, -1, count);
+    // (a host batch runs as pipelined launches of TIB_BATCH_PIPE matrices)
+    const int pipe_n = env_int("TIB_BATCH_PIPE", 16);
+    bool host_batch = true;
+    for (int k = 0; k < count; ++k) host_batch = host_batch && !ms[k]->gen.on && ms[k]->payload.pinned;
+    const int launch_n = host_batch && pipe_n > 0 && count > pipe_n ? pipe_n : count;
+    auto fp = factor_plan_for(m0.pattern, device, s, -1, launch_n);
     const Pattern& F = fp->sym.filled;
     Request req;
     req.preset = kFactorPattern;
