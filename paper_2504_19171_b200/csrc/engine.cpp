@@ -345,8 +345,8 @@ static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int 
   auto plan = std::make_shared<FactorPlan2>();
   plan->sym = symbolic_cholesky(pattern);
   plan->L = plan->sym.filled.layout();
-  // two chains keep the critical queue busier per reserved worker (tools/ab_env.py: 24 / 24 best)
-  const int crit = split > 0 ? env_int("TIB_CRIT_SPLIT_FACTOR", 24) : crit_workers(true);
+  // two chains keep the critical queue busier per reserved worker (tools/ab_env.py: 16 / 12 best)
+  const int crit = split > 0 ? env_int("TIB_CRIT_SPLIT_FACTOR", 16) : crit_workers(true);
   // the device sweep: chain task, fat leaves and the tile-boundary trick, or
   // (batches) plain leaf tasks -- the two configurations the executor is tested with
   plan->flow = upload_plan(leaves ? build_factor_dataflow(plan->sym.filled, crit, kDeferW, false, false, false, split)
@@ -1076,7 +1076,7 @@ static SigmaObj* selected_inverse_split(const MatrixObj& m, const Request& req, 
   Request preq;
   preq.preset = kFactorPattern;
   const Closure selp = symbolic_inversion(select_tiles(Fp.layout(), Fp, preq), Fp);
-  auto p2 = phase2_plan_for(Fp, selp, device, s, env_int("TIB_CRIT_SPLIT_P2", 24), sc.so.split);
+  auto p2 = phase2_plan_for(Fp, selp, device, s, env_int("TIB_CRIT_SPLIT_P2", 12), sc.so.split);
   tm.mark("plans");
   const int bp = fp->bp, N = m.layout.N;
   const size_t bb = static_cast<size_t>(bp) * bp, T = Fp.size();
@@ -2345,7 +2345,7 @@ int tib_resident_create_batch(const tib_matrix* ms, int count, int device, tib_r
     r->fp = so ? factor_plan_for(so->permuted, device, s, so->split) : factor_plan_for(m->pattern, device, s, -1, count);
     const Pattern& F = r->fp->sym.filled;
     const Closure sel = symbolic_inversion(select_tiles(F.layout(), F, req), F);
-    r->p2 = so ? phase2_plan_for(F, sel, device, s, env_int("TIB_CRIT_SPLIT_P2", 24), so->split)
+    r->p2 = so ? phase2_plan_for(F, sel, device, s, env_int("TIB_CRIT_SPLIT_P2", 12), so->split)
                : phase2_plan_for(F, sel, device, s, -1, -1, count);
     // the reference's task model counts the reference's own (natural) order
     const Closure sel_nat = symbolic_inversion(select_tiles(natural.filled.layout(), natural.filled, req), natural.filled);
