@@ -147,3 +147,25 @@ def test_no_cuda_device_fails_loudly(tib):
         pytest.skip("a GPU is present")
     with pytest.raises(tib.TileinvError, match="no CPU fallback"):
         tib.selected_inverse(tib.generate(10, 2, 1, 1.0, tile_size=2))
+
+
+def test_two_chain_order(tib):
+    """Two-chain elimination order (planner.cpp two_chain_order): a permutation
+    [I_0 ascending, I_1 descending, separator, arrow] whose symbolic fill adds
+    no tile, or none at all when the pattern does not admit one."""
+    for n, w, t, b in ((3000, 200, 30, 64), (200000, 2000, 200, 512), (100000, 1000, 100, 256), (4096, 300, 0, 128)):
+        m = tib.generate(n, w, t, 1.0, seed=1, tile_size=b)
+        order, split = tib.two_chain_order(m)
+        N = m.n_tiles
+        assert split > 0 and sorted(order.tolist()) == list(range(N))
+        # the arrow stays last (no arrow: the separator is last); I_0 is the identity prefix
+        assert order[-1] == N - 1 if t else order[-1] < N - 1
+        assert order[:split].tolist() == list(range(split))
+        # the second chain starts at the far end of the band and descends
+        assert order[split] > order[split + 1]
+        mp = tib.two_chain_permuted(m)
+        assert mp.stored_tiles == len(tib.factor_pattern(m)) == len(tib.factor_pattern(mp))
+    # too few tile columns for two interiors and a separator, and a partial last
+    # band tile with no arrow (it would fill in across the second interior)
+    assert tib.two_chain_order(tib.generate(700, 300, 0, 1.0, seed=1, tile_size=64))[1] == -1
+    assert tib.two_chain_order(tib.generate(4000, 300, 0, 1.0, seed=1, tile_size=128))[1] == -1
