@@ -262,13 +262,17 @@ static int env_int(const char* name, int dflt) {
 }
 // Streamed uploads overlap copies on one stream with the persistent sweep on
 // another, the sweep polling for the copies.  A profiler that serialises the
-// device's work (Nsight Compute injects itself through CUDA_INJECTION64_PATH)
-// would hold the copies behind the sweep and stall it until the watchdog
-// fires: then (and with TIB_STREAM_UPLOAD=0) A goes up before the sweep.
+// device's work (Nsight Compute: its injection leaves NV_COMPUTE_PROFILER_* /
+// NV_NSIGHT_INJECTION_* in the environment) would hold the copies behind the
+// sweep and stall it until the watchdog fires: then (and with
+// TIB_STREAM_UPLOAD=0) A goes up before the sweep.
 static bool streaming_allowed() {
   if (env_int("TIB_STREAM_UPLOAD", 1) == 0) return false;
-  const char* inj = std::getenv("CUDA_INJECTION64_PATH");
-  return !(inj && *inj);
+  for (const char* v : {"CUDA_INJECTION64_PATH", "NV_COMPUTE_PROFILER_PERFWORKS_DIR", "NV_NSIGHT_INJECTION_TRANSPORT_TYPE"}) {
+    const char* e = std::getenv(v);
+    if (e && *e) return false;
+  }
+  return true;
 }
 // CTAs reserved for the critical queue: the factor sweep's q0 (the chain's
 // helpers) is heavy and latency-sensitive, phase 2's (diagonal parts) is light
@@ -1067,7 +1071,8 @@ struct Unpermute {
   }
 };
 
-static SigmaObj* selected_inverse_split(const MatrixObj& m, const Request& req, int device, SplitCall& sc) {
+static SigmaObj* selected_inverse_split(const MatrixObj& m, const Request& req, int device, SplitCall& sc,
+                                        bool streamed) {
   DeviceRt& rt = runtime(device);
   cudaStream_t s = rt.stream;
   HostTimer tm(s);
@@ -1096,10 +1101,10 @@ static SigmaObj* selected_inverse_split(const MatrixObj& m, const Request& req, 
   nat->bp = bp;
   nat->nb = p2->nb;
   res->plan = nat;
-  const bool stream_up = !m.gen.on && bp == m.layout.b && m.payload.pinned && streaming_allowed() &&
-                         fp->flow->host.upl >= 0;
-  // generator output / streamed columns land here before they are placed into A
-  DevBuf staging(m.gen.on || stream_up ? sc.sel.closure.size() * bb : 0, device, s);
+  const bool host_tiles = !m.gen.on && bp == m.layout.b && m.payload.pinned;  // natural tiles copy as they are
+  const bool stream_up = streamed && host_tiles && streaming_allowed() && fp->flow->host.upl >= 0;
+  // generator output / uploaded natural tiles land here before they are placed into A
+  DevBuf staging(m.gen.on || host_tiles ? sc.sel.closure.size() * bb : 0, device, s);
   res->var = DevBuf(static_cast<size_t>(N) * bp, device, s);  // permuted order
   DevBuf& varp = res->var;
   tm.mark("allocations");
@@ -1118,6 +1123,24 @@ static SigmaObj* selected_inverse_split(const MatrixObj& m, const Request& req, 
                          reinterpret_cast<const unsigned char*>(dt.p), static_cast<int>(T), bp, 148 * 8, s);
     CK(cudaGetLastError());
     tm.mark("generate");
+    factor_sweep(*fp, st, s, tf);
+  } else if (host_tiles && !stream_up) {
+    // the natural tiles in one copy, then placed (copied / transposed) on the device
+    CK(cudaMemcpyAsync(staging.p, m.payload.p, m.pattern.size() * bb * sizeof(double), cudaMemcpyHostToDevice, s));
+    std::vector<int> d, src;
+    std::vector<unsigned char> tr;
+    for (size_t k = 0; k < T; ++k)
+      if (sc.src[k] >= 0) {
+        d.push_back(static_cast<int>(k));
+        src.push_back(sc.src[k]);
+        tr.push_back(sc.tr[k]);
+      }
+    if (d.size() < T) CK(cudaMemsetAsync(st.A.p, 0, T * bb * sizeof(double), s));  // fill-in tiles
+    DevBuf dd = to_device(d, device, s), ds = to_device(src, device, s), dt = to_device(tr, device, s);
+    launch_permute_tiles(st.A.p, staging.p, reinterpret_cast<const int*>(dd.p), reinterpret_cast<const int*>(ds.p),
+                         reinterpret_cast<const unsigned char*>(dt.p), static_cast<int>(d.size()), bp, 148 * 8, s);
+    CK(cudaGetLastError());
+    tm.mark("upload");
     factor_sweep(*fp, st, s, tf);
   } else if (!stream_up) {
     HostBuf hb(T * bb);
@@ -1236,25 +1259,27 @@ static SigmaObj* selected_inverse_split(const MatrixObj& m, const Request& req, 
 // fused factorize + phase 2 for one matrix; returns the result object
 static SigmaObj* selected_inverse_matrix(const MatrixObj& m, const Request& req, int device, bool allow_split = true) {
   // The two-chain order pays off when the factor sweep is bound by its chain:
-  // always for A already on the device (the device generator), and for a host
-  // matrix streamed up under the sweep only if the natural chain (~30 us per
-  // 64-column step) is clearly longer than the upload (~50 GB/s); otherwise
-  // the sweep waits for the upload in either order, and the split order's
-  // chains, twice as fast as the upload, leave tasks polling for columns
-  // (large config: 216 vs 203 ms).  TIB_SPLIT_STREAMED=1/0 forces it.
+  // always for A already on the device (the device generator).  A host matrix
+  // that would stream up under the sweep keeps the natural order, streamed,
+  // unless the natural chain (~30 us per 64-column step) is clearly longer
+  // than the upload (~50 GB/s) -- otherwise the sweep waits for the upload in
+  // either order (large config) -- and then goes up before the split sweep
+  // and is placed on the device (medium: 82 -> ~72 ms).  TIB_SPLIT_STREAMED=1
+  // streams the split order (in-kernel placement agents; a rare stall with
+  // 8 agents is unresolved, so it is not the default).
   const bool streams = !m.gen.on && m.payload.pinned && m.layout.b % 64 == 0 && streaming_allowed();
-  bool split_ok = !streams;
-  if (streams) {
-    const int forced = env_int("TIB_SPLIT_STREAMED", -1);
+  const int forced = env_int("TIB_SPLIT_STREAMED", 0);
+  bool split_ok = !streams || forced != 0;
+  if (streams && !split_ok) {
     const double chain_ms = m.layout.N * ((m.layout.b + 63) / 64) * 0.030;
     const double upload_ms = static_cast<double>(m.pattern.size()) * m.layout.b * m.layout.b * 8 / 50e6;
-    split_ok = forced >= 0 ? forced != 0 : chain_ms > 1.3 * upload_ms;
+    split_ok = chain_ms > 1.3 * upload_ms;
   }
   if (allow_split && split_ok) {
     SplitCall sc;
     if (split_call(m, req, sc)) {
       try {
-        return selected_inverse_split(m, req, device, sc);
+        return selected_inverse_split(m, req, device, sc, streams && forced != 0);
       } catch (const NotSpd&) {
         // the failing pivot of the permuted elimination is not the reference's:
         // the natural order reports the first non-positive pivot like factorize

@@ -126,6 +126,7 @@ def test_factor_path_and_determinism(tib, orc, monkeypatch):
     assert abs(f.logdet() - ref["logdet"]) <= TOL * abs(ref["logdet"])
     via = tib.selected_inverse_of_factor(f, "pattern")
     monkeypatch.setenv("TIB_SPLIT_STREAMED", "1")  # the two-chain order, streamed
+    monkeypatch.setenv("TIB_SPLIT_AGENTS", "1")
     direct = tib.selected_inverse(m, "pattern")
     again = tib.selected_inverse(m, "pattern")
     # fixed accumulation order, no atomics on data: bitwise reproducible
@@ -170,6 +171,7 @@ def test_streamed_upload_is_bitwise_identical(tib, monkeypatch, split):
     in either elimination order."""
     monkeypatch.setenv("TIB_SPLIT", split)
     monkeypatch.setenv("TIB_SPLIT_STREAMED", split)
+    monkeypatch.setenv("TIB_SPLIT_AGENTS", "1")
     m = tib.generate(6000, 700, 60, 1.0, seed=23, tile_size=256)
     streamed = tib.selected_inverse(m, "pattern")
     monkeypatch.setenv("TIB_STREAM_UPLOAD", "0")
@@ -191,6 +193,7 @@ def test_two_chain_order_matches_natural(tib, orc, monkeypatch, how):
         monkeypatch.setenv("TIB_STREAM_UPLOAD", "0")
     if how == "streamed":  # host inputs stream in the natural order unless asked
         monkeypatch.setenv("TIB_SPLIT_STREAMED", "1")
+        monkeypatch.setenv("TIB_SPLIT_AGENTS", "1")
     got = tib.selected_inverse(m, "pattern")
     monkeypatch.setenv("TIB_SPLIT", "0")
     nat = tib.selected_inverse(m, "pattern")

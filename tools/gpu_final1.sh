@@ -1,0 +1,12 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out/final1
+nvidia-smi --query-gpu=name,clocks.max.sm,power.limit --format=csv > gpurun_out/final1/smi.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final1/smoke.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/final1/tests.log 2>&1
+timeout 600 python bench.py > gpurun_out/final1/bench_large.json 2> gpurun_out/final1/bench_large.err
+for c in medium batch kronecker; do
+  timeout 600 python bench.py --config $c > gpurun_out/final1/bench_$c.json 2> gpurun_out/final1/bench_$c.err
+done
+timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/final1/ref_large.json 2>&1
+CUDA_INJECTION64_PATH= timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/final1/launches_smoke.csv python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final1/smoke_ncu.log 2>&1
+timeout 1500 ncu --set full --import-source on --clock-control none -k regex:dataflow_kernel --launch-skip 1 -c 1 -o gpurun_out/final1/phase2_large python tools/prof_run.py large 1 > gpurun_out/final1/ncu_p2.log 2>&1
