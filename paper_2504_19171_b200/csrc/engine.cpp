@@ -1,25 +1,24 @@
 // Host engine of the B200 path: builds pointer-free task plans from the
-// symbolic planner, owns device stores, runs the two column sweeps on a CUDA
-// stream (captured once into a CUDA graph per plan), and implements the C ABI
-// declared in include/tileinv_b200.h.
+// symbolic planner (plan.cpp), owns device stores, runs the two sweeps -- each
+// one launch of the persistent dataflow executor (kernels.cu), captured into a
+// CUDA graph per plan and batch size -- and implements the C ABI declared in
+// include/tileinv_b200.h.
 //
-// Device data layout: every store is one contiguous
-// allocation of `tiles x bp x bp` doubles in pattern slot order (column-major
-// over the tile grid, diagonal first in each column), bp = b rounded up to 64
-// with identity padding on diagonal tiles.  Stores: A (working copy, Schur
-// updates in place), L (factor), P1 (X_j = L_jj^{-1} on diagonal slots,
-// W_kj = L_kj X_j off them), Sigma (closure slots), Var (N x bp marginal
-// variances), Scratch, Logdet (N x bp/64 partial sums).
+// Device data layout: every store is one contiguous allocation
+// of `tiles x bp x bp` doubles in pattern slot order (column-major over the
+// tile grid, diagonal first in each column), bp = b rounded up to 64 with
+// identity padding on diagonal tiles.  Stores: A (working copy, Schur updates
+// in place), L (factor), P1 (X_j = L_jj^{-1} on diagonal slots, W_kj = L_kj X_j
+// off them), Sigma (closure slots), Var (N x bp marginal variances), Scratch
+// (T-term accumulators, split-K partials), Logdet (N x bp/64 partial sums),
+// Counters (dependency, arrival and upload counters).
 //
-// Column sweep (fused factorization + phase 1), per column j, in order:
-//   diag_cluster_kernel : L_jj = chol(A_jj), X_j = L_jj^{-1}         (potrf_tile + trtri_tile)
-//   gemm tasks          : L_kj = A_kj X_j^T  for k in nb(j), k > j     (trsm_tile recast)
-//   gemm tasks          : W_kj = L_kj X_j                               (trmm_tile, phase 1)
-//                         A_ab -= L_aj L_bj^T, a >= b in nb(j) > j      (syrk_tile / gemm_tile)
-// Phase-2 sweep, per closure column i descending (selinv.cpp:239-345):
-//   gemm tasks          : Sigma_ji = -sum_k M_jk W_ki                   (gemm_tile, off-diagonal)
-//   gemm tasks          : Sigma_ii = X_i^T X_i - sum_k W_ki^T Sigma_ki  (lauum_tile + gemm_tile),
-//                         mirrored exactly, diag -> Var
+// Sweeps: the fused factorization + phase 1 (64x64 block tasks:
+// the diagonal chain, panels L_kj = A_kj X_j^T, Schur updates, W_kj), then
+// phase 2 per closure column descending (selinv.cpp:239-345).  Single-matrix
+// calls run in the two-chain elimination order when it pays off
+// (selected_inverse_split); host inputs stream up under the factor sweep;
+// batches are one launch per sweep (or pipelined groups for host batches).
 #include <cuda_runtime.h>
 
 #include <algorithm>
