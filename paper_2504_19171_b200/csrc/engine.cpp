@@ -323,6 +323,16 @@ static std::mutex g_plan_mu;
 static std::map<std::pair<int, uint64_t>, std::shared_ptr<FactorPlan2>> g_fplans;
 static std::map<std::pair<int, uint64_t>, std::shared_ptr<Phase2Plan>> g_p2plans;
 
+// Update work per elimination step relative to the chain: (tiles per column)^2
+// x (blocks per tile)^2.  Above TIB_SPLIT_WORK the sweeps are throughput bound
+// even with one chain (Kronecker), below it a single chain bounds them.
+static double chain_work(const Pattern& F) {
+  const int N = F.layout().N;
+  const double per_col = static_cast<double>(F.size() - static_cast<size_t>(N)) / N;
+  const double nbk = static_cast<double>((F.layout().b + 63) / 64);
+  return per_col * per_col * nbk * nbk;
+}
+
 // batch > 4 (chains share their SMs): no chain task.  A batch is throughput
 // bound; a chain task would tie one worker per matrix for the whole sweep
 // (64 x 157 ms at config 5, ~11 % of it computing) and its fat steps wait in
@@ -348,8 +358,12 @@ static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int 
   auto plan = std::make_shared<FactorPlan2>();
   plan->sym = symbolic_cholesky(pattern);
   plan->L = plan->sym.filled.layout();
-  // two chains keep the critical queue busier per reserved worker (tools/ab_env.py: 16 / 12 best)
-  const int crit = split > 0 ? env_int("TIB_CRIT_SPLIT_FACTOR", 16) : crit_workers(true);
+  // two chains keep the critical queue busier per reserved worker (tools/ab_env.py: 16 / 12 best);
+  // a throughput-bound single chain (chain work above TIB_SPLIT_WORK: Kronecker) needs few
+  // (Kronecker factor sweep 276 -> 248 ms at 8)
+  const bool tput = chain_work(plan->sym.filled) > env_int("TIB_SPLIT_WORK", 3000);
+  const int crit = split > 0 ? env_int("TIB_CRIT_SPLIT_FACTOR", 16)
+                             : (tput ? env_int("TIB_CRIT_TPUT_FACTOR", 8) : crit_workers(true));
   // the device sweep: chain task, fat leaves and the tile-boundary trick, or
   // (batches) plain leaf tasks -- the two configurations the executor is tested with
   plan->flow = upload_plan(leaves ? build_factor_dataflow(plan->sym.filled, crit, kDeferW, false, false, false, split)
@@ -372,16 +386,6 @@ static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int 
 // larger parts win (two-chain large 101.3 -> 99.8 ms, batch 137 -> 128 ms at
 // 3); a single chain is latency-bound there (natural-order large 101.8 ->
 // 117.5 ms, two-chain medium 17 -> 27 ms at 3), so one term per part.
-// Update work per elimination step relative to the chain: (tiles per column)^2
-// x (blocks per tile)^2.  Above TIB_SPLIT_WORK the sweeps are throughput bound
-// even with one chain (Kronecker), below it a single chain bounds them.
-static double chain_work(const Pattern& F) {
-  const int N = F.layout().N;
-  const double per_col = static_cast<double>(F.size() - static_cast<size_t>(N)) / N;
-  const double nbk = static_cast<double>((F.layout().b + 63) / 64);
-  return per_col * per_col * nbk * nbk;
-}
-
 static int phase2_group(const Pattern& F, int batch, int split) {
   const int forced = env_int("TIB_P2_GROUP", 0);
   if (forced > 0) return forced;
@@ -392,7 +396,8 @@ static int phase2_group(const Pattern& F, int batch, int split) {
 
 static std::shared_ptr<Phase2Plan> phase2_plan_for(const Pattern& F, const Closure& sel, int device,
                                                    cudaStream_t s, int crit = -1, int split = -1, int batch = 1) {
-  if (crit < 0) crit = crit_workers(false);
+  if (crit < 0)
+    crit = chain_work(F) > env_int("TIB_SPLIT_WORK", 3000) ? env_int("TIB_CRIT_TPUT_P2", 6) : crit_workers(false);
   const int group = phase2_group(F, batch, split);
   const uint64_t key = pattern_hash(
       sel.closure, pattern_hash(F, 2 + 7919ull * static_cast<uint64_t>(crit) + 104729ull * static_cast<uint64_t>(split + 2) +
