@@ -394,6 +394,13 @@ static int phase2_group(const Pattern& F, int batch, int split) {
   return throughput ? 3 : 1;
 }
 
+// Reserved critical workers of a two-chain phase-2 plan: a throughput-bound
+// phase 2 (late terms grouped) needs few (large: 12 vs 24, 98.7 vs 99.8 ms), a
+// chain-bound one more (medium: 24 vs 12, 16.9 vs 17.7 ms).
+static int crit_split_p2(const Pattern& F, int split) {
+  return env_int("TIB_CRIT_SPLIT_P2", phase2_group(F, 1, split) > 1 ? 12 : 24);
+}
+
 static std::shared_ptr<Phase2Plan> phase2_plan_for(const Pattern& F, const Closure& sel, int device,
                                                    cudaStream_t s, int crit = -1, int split = -1, int batch = 1) {
   if (crit < 0)
@@ -1085,7 +1092,7 @@ static SigmaObj* selected_inverse_split(const MatrixObj& m, const Request& req, 
   Request preq;
   preq.preset = kFactorPattern;
   const Closure selp = symbolic_inversion(select_tiles(Fp.layout(), Fp, preq), Fp);
-  auto p2 = phase2_plan_for(Fp, selp, device, s, env_int("TIB_CRIT_SPLIT_P2", 12), sc.so.split);
+  auto p2 = phase2_plan_for(Fp, selp, device, s, crit_split_p2(Fp, sc.so.split), sc.so.split);
   tm.mark("plans");
   const int bp = fp->bp, N = m.layout.N;
   const size_t bb = static_cast<size_t>(bp) * bp, T = Fp.size();
@@ -2374,7 +2381,7 @@ int tib_resident_create_batch(const tib_matrix* ms, int count, int device, tib_r
     r->fp = so ? factor_plan_for(so->permuted, device, s, so->split) : factor_plan_for(m->pattern, device, s, -1, count);
     const Pattern& F = r->fp->sym.filled;
     const Closure sel = symbolic_inversion(select_tiles(F.layout(), F, req), F);
-    r->p2 = so ? phase2_plan_for(F, sel, device, s, env_int("TIB_CRIT_SPLIT_P2", 12), so->split)
+    r->p2 = so ? phase2_plan_for(F, sel, device, s, crit_split_p2(F, so->split), so->split)
                : phase2_plan_for(F, sel, device, s, -1, -1, count);
     // the reference's task model counts the reference's own (natural) order
     const Closure sel_nat = symbolic_inversion(select_tiles(natural.filled.layout(), natural.filled, req), natural.filled);
