@@ -367,7 +367,8 @@ static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int 
   // the device sweep: chain task, fat leaves and the tile-boundary trick, or
   // (batches) plain leaf tasks -- the two configurations the executor is tested with
   plan->flow = upload_plan(leaves ? build_factor_dataflow(plan->sym.filled, crit, kDeferW, false, false, false, split)
-                                  : build_factor_dataflow(plan->sym.filled, crit, kDeferW, true, true, true, split),
+                                  : build_factor_dataflow(plan->sym.filled, crit, kDeferW, true, true, true, split,
+                                                          env_int("TIB_COARSE_SECOND", 1) != 0),
                            device, s);
   // reserved critical workers of launches without dedicated chain SMs: more
   // for leaf tasks (the whole chain goes through the critical queue)
@@ -2306,7 +2307,8 @@ int tib_plan_export(tib_matrix m, int preset, const long* rows, const long* cols
       // the CPU simulator runs the same decomposition as the GPU chain, with the
       // chain's steps kept as (fat / boundary) leaf tasks
       P = batch_leaves(batch) ? build_factor_dataflow(sym.filled, crit_workers, kDeferW, false, false, false, split)
-                              : build_factor_dataflow(sym.filled, crit_workers, kDeferW, true, false, true, split);
+                              : build_factor_dataflow(sym.filled, crit_workers, kDeferW, true, false, true, split,
+                                                      env_int("TIB_COARSE_SECOND", 1) != 0);
     } else {
       const Closure sel =
           symbolic_inversion(select_tiles(sym.filled.layout(), sym.filled, make_request(preset, rows, cols, ne)), sym.filled);

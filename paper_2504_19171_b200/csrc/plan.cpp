@@ -222,7 +222,7 @@ void validate_dataflow(const DataflowPlan& plan, const std::vector<int>& order) 
 }
 
 DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer_w, bool fat_leaf, bool chain,
-                                   bool boundary, int split) {
+                                   bool boundary, int split, bool coarse_second) {
   if (chain) fat_leaf = true;
   if (boundary) fat_leaf = true;
   DataflowPlan P;
@@ -674,7 +674,8 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
         if (kk + 1 < nb) s_tasks(kk + 1);
       }
     }
-    if (tail1) {
+    const bool coarse1 = two && coarse_second;
+    if (tail1 && !coarse1) {
       // second tile: same progression, issued on the bulk queue right after the chain
       for (int kk = 0; kk < nb; ++kk) {
         panel_prog(1, kk, 1, panel_slots);
@@ -697,11 +698,10 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
           B.seg(t, kStoreA, tile_off(sk, bp), kStoreP1, tile_off(ds, bp), 0, (q + 1) * kB, kTransB);
         }
     };
-    auto update = [&](size_t ia, size_t ic) {
+    auto update_with = [&](size_t ia, size_t ic, int u) {
       const int a = krows[ia], c = krows[ic];
       const long ts = F.slot(a, c);
       if (ts < 0) throw Error(kErrConsistency, "update target outside the filled pattern");
-      const int u = ord[static_cast<size_t>(ts)]++;
       for (int p = 0; p < nb; ++p)
         for (int q = 0; q < (a == c ? p + 1 : nb); ++q) {
           std::vector<int> sg{aord(ts, p, q)};
@@ -715,6 +715,18 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
           B.seg(t, kStoreL, tile_off(ks[ia], bp), kStoreL, tile_off(ks[ic], bp), 0, bp, kTransB | kNegate);
         }
     };
+    auto update = [&](size_t ia, size_t ic) {
+      const long ts = F.slot(krows[ia], krows[ic]);
+      if (ts < 0) throw Error(kErrConsistency, "update target outside the filled pattern");
+      update_with(ia, ic, ord[static_cast<size_t>(ts)]++);
+    };
+    // two chains (the sweep is throughput-bound, not chain-bound): the second
+    // tile's panel and its update of tile (k1, k0) as whole-K bulk tasks
+    // instead of the progressive split-K parts
+    if (tail1 && coarse1) {
+      panel(1);
+      update_with(1, 0, u10);
+    }
     for (size_t ia = 2; ia < krows.size(); ++ia) panel(ia);
     for (size_t ia = 2; ia < krows.size(); ++ia) update(ia, 0);
     for (size_t ic = 1; ic < krows.size(); ++ic)

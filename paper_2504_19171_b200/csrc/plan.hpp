@@ -61,8 +61,11 @@ struct DataflowPlan {
 // split > 0: columns [split, N) form a second elimination chain independent of
 // [0, split) until they meet (two_chain_order): two chain tasks, one scratch
 // ring each.
+// coarse_second (with split): the second off-diagonal tile's panel and update
+// as whole-K bulk tasks instead of the progressive split-K parts.
 DataflowPlan build_factor_dataflow(const Pattern& filled, int crit_workers, int defer_w, bool fat_leaf,
-                                   bool chain = false, bool boundary = false, int split = -1);
+                                   bool chain = false, bool boundary = false, int split = -1,
+                                   bool coarse_second = false);
 
 // Phase 1 alone (selinv.cpp:195-237) from a given factor L (a factor read back
 // from a tile file): X_j = L_jj^{-1} and W_kj = L_kj X_j, every column
