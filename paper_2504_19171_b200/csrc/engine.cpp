@@ -345,11 +345,25 @@ static bool batch_leaves(int batch) {
   return batch >= env_int("TIB_BATCH_LEAVES_MIN", 32) && env_int("TIB_BATCH_CHAIN", 0) == 0;
 }
 
+// Bulk update terms per factor task (build_factor_dataflow's ugroup): four
+// terms to a multi-segment GEMM (K = 4 bp), except in a single natural-order
+// chain that bounds its sweep (each term as early as its column: large
+// natural order 93.8 vs 95.6 ms grouped).  tools/ab_env.py, one B200: factor
+// sweep large 85.8 -> 81.1 ms, Kronecker 248 -> 229, batch 131.5 -> 113.9,
+// medium 29.0 -> 27.5 (flat from 4 to 16 terms).
+static int factor_update_group(const Pattern& F, int batch, int split) {
+  const int forced = env_int("TIB_UPD_GROUP", 0);
+  if (forced > 0) return forced;
+  const bool chain_bound = split <= 0 && !batch_leaves(batch) && chain_work(F) <= env_int("TIB_SPLIT_WORK", 3000);
+  return chain_bound ? 1 : 4;
+}
+
 static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int device, cudaStream_t s,
                                                     int split = -1, int batch = 1) {
   const bool leaves = batch_leaves(batch);
+  const int ug = factor_update_group(pattern, batch, split);  // on the input pattern (cache key)
   const uint64_t key = pattern_hash(pattern, 1 + 0x9e3779b97f4a7c15ull * static_cast<uint64_t>(split + 2) +
-                                                 (leaves ? 0x51ed27ull : 0));
+                                                 (leaves ? 0x51ed27ull : 0) + 0x2545f491ull * static_cast<uint64_t>(ug));
   {
     std::lock_guard<std::mutex> lk(g_plan_mu);
     auto it = g_fplans.find({device, key});
@@ -366,9 +380,10 @@ static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int 
                              : (tput ? env_int("TIB_CRIT_TPUT_FACTOR", 8) : crit_workers(true));
   // the device sweep: chain task, fat leaves and the tile-boundary trick, or
   // (batches) plain leaf tasks -- the two configurations the executor is tested with
-  plan->flow = upload_plan(leaves ? build_factor_dataflow(plan->sym.filled, crit, kDeferW, false, false, false, split)
+  plan->flow = upload_plan(leaves ? build_factor_dataflow(plan->sym.filled, crit, kDeferW, false, false, false, split,
+                                                          false, ug)
                                   : build_factor_dataflow(plan->sym.filled, crit, kDeferW, true, true, true, split,
-                                                          env_int("TIB_COARSE_SECOND", 1) != 0),
+                                                          env_int("TIB_COARSE_SECOND", 1) != 0, ug),
                            device, s);
   // reserved critical workers of launches without dedicated chain SMs: more
   // for leaf tasks (the whole chain goes through the critical queue)
@@ -2306,9 +2321,11 @@ int tib_plan_export(tib_matrix m, int preset, const long* rows, const long* cols
     if (which == 0) {
       // the CPU simulator runs the same decomposition as the GPU chain, with the
       // chain's steps kept as (fat / boundary) leaf tasks
-      P = batch_leaves(batch) ? build_factor_dataflow(sym.filled, crit_workers, kDeferW, false, false, false, split)
+      const int ug = factor_update_group(m->pattern, batch, split);
+      P = batch_leaves(batch) ? build_factor_dataflow(sym.filled, crit_workers, kDeferW, false, false, false, split,
+                                                      false, ug)
                               : build_factor_dataflow(sym.filled, crit_workers, kDeferW, true, false, true, split,
-                                                      env_int("TIB_COARSE_SECOND", 1) != 0);
+                                                      env_int("TIB_COARSE_SECOND", 1) != 0, ug);
     } else {
       const Closure sel =
           symbolic_inversion(select_tiles(sym.filled.layout(), sym.filled, make_request(preset, rows, cols, ne)), sym.filled);

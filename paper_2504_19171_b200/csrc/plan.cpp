@@ -222,7 +222,7 @@ void validate_dataflow(const DataflowPlan& plan, const std::vector<int>& order) 
 }
 
 DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer_w, bool fat_leaf, bool chain,
-                                   bool boundary, int split, bool coarse_second) {
+                                   bool boundary, int split, bool coarse_second, int ugroup) {
   if (chain) fat_leaf = true;
   if (boundary) fat_leaf = true;
   DataflowPlan P;
@@ -310,6 +310,43 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
   P.slot_tiles = F.tiles();
   Builder B(P);
   std::vector<int> ord(static_cast<size_t>(T), 0);  // update columns applied so far, per tile
+  // grouped bulk updates (ugroup > 1): pending terms (source slots of L(a, k),
+  // L(c, k)) per target slot, emitted as one multi-segment task per block with
+  // ordinals ord .. ord + terms - 1 (its signals are repeated once per term, so
+  // every waiter on an intermediate count is still woken)
+  std::vector<std::vector<std::pair<long, long>>> pend(ugroup > 1 ? static_cast<size_t>(T) : 0);
+  auto flush = [&](long ts) {
+    if (ugroup <= 1 || ts < 0) return;
+    auto& terms = pend[static_cast<size_t>(ts)];
+    if (terms.empty()) return;
+    const Coord tc = F.tiles()[static_cast<size_t>(ts)];
+    const int u = ord[static_cast<size_t>(ts)];
+    const int n = static_cast<int>(terms.size());
+    ord[static_cast<size_t>(ts)] += n;
+    for (int p = 0; p < nb; ++p)
+      for (int q = 0; q < (tc.i == tc.j ? p + 1 : nb); ++q) {
+        std::vector<Dep> d;
+        for (const auto& tm : terms) {
+          d.push_back({lfin(tm.first), NB2});
+          if (tm.second != tm.first) d.push_back({lfin(tm.second), NB2});
+        }
+        d.push_back({aord(ts, p, q), u});
+        std::vector<int> sg;
+        for (int x = 0; x < n; ++x) {
+          sg.push_back(aord(ts, p, q));
+          if (tc.i != tc.j) sg.push_back(afin(ts));
+        }
+        DTask& t = B.add(1, d, sg);
+        t.kind = kGemmTask;
+        t.c_store = t.c0_store = kStoreA;
+        t.c_off = t.c0_off = blk_off(ts, bp, p, q);
+        t.m0 = p * kB;
+        t.n0 = q * kB;
+        for (const auto& tm : terms)
+          B.seg(t, kStoreL, tile_off(tm.first, bp), kStoreL, tile_off(tm.second, bp), 0, bp, kTransB | kNegate);
+      }
+    terms.clear();
+  };
 
   auto emit_w = [&](int j) {
     const long ds = F.col_start(j);
@@ -331,9 +368,7 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
 
   std::vector<int> ring_count(static_cast<size_t>(N), 0);
   for (int j = 0; j < N; ++j) {
-    const size_t col_first = B.all.size();
     const long ds = F.col_start(j);
-    const int U = ord[static_cast<size_t>(ds)];
     const int valid = static_cast<int>(std::min<long>(L.b, L.n - static_cast<long>(j) * L.b));
     std::vector<int> krows;
     std::vector<long> ks;
@@ -342,6 +377,15 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
         krows.push_back(*r);
         ks.push_back(F.slot(*r, j));
       }
+    // every tile this column reads or updates outside the grouped bulk terms
+    if (ugroup > 1) {
+      flush(ds);
+      for (long sk : ks) flush(sk);
+      if (!krows.empty()) flush(F.slot(krows[0], krows[0]));
+      if (krows.size() > 1) flush(F.slot(krows[1], krows[0]));
+    }
+    const size_t col_first = B.all.size();
+    const int U = ord[static_cast<size_t>(ds)];
     // first off-diagonal tile of the column and its update ordinals (the
     // progressive tail below), needed by the boundary leaf
     const bool tail0 = !krows.empty(), tail1 = krows.size() > 1;
@@ -718,6 +762,12 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
     auto update = [&](size_t ia, size_t ic) {
       const long ts = F.slot(krows[ia], krows[ic]);
       if (ts < 0) throw Error(kErrConsistency, "update target outside the filled pattern");
+      if (ugroup > 1) {
+        auto& terms = pend[static_cast<size_t>(ts)];
+        terms.emplace_back(ks[ia], ks[ic]);
+        if (static_cast<int>(terms.size()) >= ugroup) flush(ts);
+        return;
+      }
       update_with(ia, ic, ord[static_cast<size_t>(ts)]++);
     };
     // two chains (the sweep is throughput-bound, not chain-bound): the second
@@ -758,6 +808,7 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
     if (j - defer_w >= 0) emit_w(j - defer_w);
   }
   for (int j = std::max(0, N - defer_w); j < N; ++j) emit_w(j);
+  for (long ts = 0; ts < (ugroup > 1 ? T : 0); ++ts) flush(ts);  // none left on a consistent pattern
   // streamed upload: each task polls the upload counter of the latest tile
   // column of A it reads or writes
   {

@@ -63,9 +63,13 @@ struct DataflowPlan {
 // ring each.
 // coarse_second (with split): the second off-diagonal tile's panel and update
 // as whole-K bulk tasks instead of the progressive split-K parts.
+// ugroup > 1: the bulk updates of a tile are grouped, up to ugroup terms
+// (ascending column) per task -- one multi-segment GEMM of K = ugroup * bp
+// instead of ugroup K = bp tasks; a tile's pending terms go out before the
+// tile's next non-bulk use (its panel, leaf or critical split update).
 DataflowPlan build_factor_dataflow(const Pattern& filled, int crit_workers, int defer_w, bool fat_leaf,
                                    bool chain = false, bool boundary = false, int split = -1,
-                                   bool coarse_second = false);
+                                   bool coarse_second = false, int ugroup = 1);
 
 // Phase 1 alone (selinv.cpp:195-237) from a given factor L (a factor read back
 // from a tile file): X_j = L_jj^{-1} and W_kj = L_kj X_j, every column

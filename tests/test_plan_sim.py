@@ -159,3 +159,25 @@ def test_plan_simulation_batch_plans(tib, orc, case, order):
     assert closure == ref["tiles"]
     assert normwise(sig, ref["payload"]) <= 1e-12
     assert abs(logdet - ref["logdet"]) <= 1e-12 * abs(ref["logdet"])
+
+
+@pytest.mark.parametrize("group", [2, 3, 5])
+@pytest.mark.parametrize("case", [
+    (700, 90, 12, 1.0, 5, 64, "pattern"),      # band 2 tiles: groups cut by the tile's next use
+    (1100, 300, 40, 1.0, 9, 64, "pattern"),    # band 5 tiles: full groups
+    (1000, 0, 100, 1.0, 4, 100, "pattern"),    # arrow only
+], ids=lambda c: str(c[:6]) if isinstance(c, tuple) else str(c))
+@pytest.mark.parametrize("order", [None, 1])
+def test_plan_simulation_grouped_updates(tib, orc, monkeypatch, case, group, order):
+    """Bulk update terms grouped `group` to a factor task (multi-segment GEMMs,
+    signals repeated per term) in the chain plan, a batch plan and a random
+    ready order: Sigma and logdet still equal the oracle's."""
+    monkeypatch.setenv("TIB_UPD_GROUP", str(group))
+    n, w, t, d, seed, b, sel = case
+    m = tib.generate(n, w, t, d, seed=seed, tile_size=b)
+    ref = orc.selected_inverse_generated(n, w, t, d, seed, b, sel)
+    for batch in (1, 64):
+        _, closure, sig, logdet, _, var = run_plans(tib, m, sel, order=order, batch=batch)
+        assert closure == ref["tiles"]
+        assert normwise(sig, ref["payload"]) <= 1e-12
+        assert abs(logdet - ref["logdet"]) <= 1e-12 * abs(ref["logdet"])
