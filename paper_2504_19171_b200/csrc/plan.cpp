@@ -90,9 +90,14 @@ struct Builder {
       P.chain.clear();
       conv.assign(all.size(), -1);
       const bool any_leaf = std::any_of(all.begin(), all.end(), [](const DTask& t) { return t.kind == kLeafTask; });
+      // (two chains: the first chain's leaves, then the second's -- the
+      // columns may be emitted interleaved)
+      for (int pass = 0; pass < (split > 0 ? 2 : 1); ++pass)
+        for (size_t i = 0; i < all.size(); ++i)
+          if (all[i].kind == kLeafTask && (split <= 0 || (all[i].n0 / P.L.b >= split) == (pass == 1)))
+            P.chain.push_back(all[i]);
       for (size_t i = 0; i < all.size(); ++i) {
         if (all[i].kind == kLeafTask) {
-          P.chain.push_back(all[i]);
         } else {
           conv[i] = static_cast<int>(rest.size()) + (any_leaf ? 1 : 0);
           rest.push_back(all[i]);
@@ -100,7 +105,7 @@ struct Builder {
         }
       }
       // one chain task per elimination chain: steps of columns < split, then
-      // the rest (the leaves are emitted in column order)
+      // the rest (partitioned by chain above, column order within each)
       std::vector<int> bounds{0};
       if (split > 0) {
         int k = 0;
@@ -367,7 +372,26 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
   };
 
   std::vector<int> ring_count(static_cast<size_t>(N), 0);
-  for (int j = 0; j < N; ++j) {
+  // emission order of the columns: ascending, or -- two chains -- the chains'
+  // columns interleaved by elimination step (column k runs at step k, or
+  // k - split in the second chain).  Update ordinals follow emission order, so
+  // a tile both chains update (separator, arrow) takes their terms in the order
+  // they become available instead of all of the first chain's before any of
+  // the second's (which serialised ~190 arrow-tip terms after the first chain
+  // ended: the last ~7 ms of the large config's factor sweep).
+  std::vector<int> seq;
+  seq.reserve(static_cast<size_t>(N));
+  if (two) {
+    int a = 0, c = split;
+    while (a < split || c < N) {
+      if (c >= N || (a < split && a <= c - split)) seq.push_back(a++);
+      else seq.push_back(c++);
+    }
+  } else {
+    for (int j = 0; j < N; ++j) seq.push_back(j);
+  }
+  for (int jx = 0; jx < N; ++jx) {
+    const int j = seq[static_cast<size_t>(jx)];
     const long ds = F.col_start(j);
     const int valid = static_cast<int>(std::min<long>(L.b, L.n - static_cast<long>(j) * L.b));
     std::vector<int> krows;
@@ -805,9 +829,9 @@ DataflowPlan build_factor_dataflow(const Pattern& F, int crit_workers, int defer
           if (writer) B.add_dep(t, {ringdone(prev), ring_count[static_cast<size_t>(prev)]});
         }
     }
-    if (j - defer_w >= 0) emit_w(j - defer_w);
+    if (jx - defer_w >= 0) emit_w(seq[static_cast<size_t>(jx - defer_w)]);
   }
-  for (int j = std::max(0, N - defer_w); j < N; ++j) emit_w(j);
+  for (int jx = std::max(0, N - defer_w); jx < N; ++jx) emit_w(seq[static_cast<size_t>(jx)]);
   for (long ts = 0; ts < (ugroup > 1 ? T : 0); ++ts) flush(ts);  // none left on a consistent pattern
   // streamed upload: each task polls the upload counter of the latest tile
   // column of A it reads or writes
