@@ -361,9 +361,11 @@ static int factor_update_group(const Pattern& F, int batch, int split) {
 static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int device, cudaStream_t s,
                                                     int split = -1, int batch = 1) {
   const bool leaves = batch_leaves(batch);
-  const int ug = factor_update_group(pattern, batch, split);  // on the input pattern (cache key)
+  // (the grouping is a function of the filled pattern, batch and split; only a
+  // forced TIB_UPD_GROUP needs to be in the key)
   const uint64_t key = pattern_hash(pattern, 1 + 0x9e3779b97f4a7c15ull * static_cast<uint64_t>(split + 2) +
-                                                 (leaves ? 0x51ed27ull : 0) + 0x2545f491ull * static_cast<uint64_t>(ug));
+                                                 (leaves ? 0x51ed27ull : 0) +
+                                                 0x2545f491ull * static_cast<uint64_t>(env_int("TIB_UPD_GROUP", 0)));
   {
     std::lock_guard<std::mutex> lk(g_plan_mu);
     auto it = g_fplans.find({device, key});
@@ -372,11 +374,12 @@ static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int 
   auto plan = std::make_shared<FactorPlan2>();
   plan->sym = symbolic_cholesky(pattern);
   plan->L = plan->sym.filled.layout();
+  const int ug = factor_update_group(plan->sym.filled, batch, split);
   // two chains keep the critical queue busier per reserved worker (tools/ab_env.py: 16 / 12 best);
   // a throughput-bound single chain (chain work above TIB_SPLIT_WORK: Kronecker) needs few
   // (Kronecker factor sweep 276 -> 248 ms at 8)
   const bool tput = chain_work(plan->sym.filled) > env_int("TIB_SPLIT_WORK", 3000);
-  const int crit = split > 0 ? env_int("TIB_CRIT_SPLIT_FACTOR", 16)
+  const int crit = split > 0 ? env_int("TIB_CRIT_SPLIT_FACTOR", 24)
                              : (tput ? env_int("TIB_CRIT_TPUT_FACTOR", 8) : crit_workers(true));
   // the device sweep: chain task, fat leaves and the tile-boundary trick, or
   // (batches) plain leaf tasks -- the two configurations the executor is tested with
@@ -2323,7 +2326,7 @@ int tib_plan_export(tib_matrix m, int preset, const long* rows, const long* cols
     if (which == 0) {
       // the CPU simulator runs the same decomposition as the GPU chain, with the
       // chain's steps kept as (fat / boundary) leaf tasks
-      const int ug = factor_update_group(m->pattern, batch, split);
+      const int ug = factor_update_group(sym.filled, batch, split);
       P = batch_leaves(batch) ? build_factor_dataflow(sym.filled, crit_workers, kDeferW, false, false, false, split,
                                                       false, ug)
                               : build_factor_dataflow(sym.filled, crit_workers, kDeferW, true, false, true, split,
