@@ -375,7 +375,8 @@ static std::shared_ptr<FactorPlan2> factor_plan_for(const Pattern& pattern, int 
   plan->sym = symbolic_cholesky(pattern);
   plan->L = plan->sym.filled.layout();
   const int ug = factor_update_group(plan->sym.filled, batch, split);
-  // two chains keep the critical queue busier per reserved worker (tools/ab_env.py: 16 / 12 best);
+  // two chains keep the critical queue busier per reserved worker (tools/ab_env.py: 24 / 12 best with
+  // grouped updates, profiles/r02_s4_ab_crit.log);
   // a throughput-bound single chain (chain work above TIB_SPLIT_WORK: Kronecker) needs few
   // (Kronecker factor sweep 276 -> 248 ms at 8)
   const bool tput = chain_work(plan->sym.filled) > env_int("TIB_SPLIT_WORK", 3000);
