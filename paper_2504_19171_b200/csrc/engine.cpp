@@ -353,7 +353,7 @@ static bool batch_leaves(int batch) {
 // medium 29.0 -> 27.5 (flat from 4 to 16 terms).
 static int factor_update_group(const Pattern& F, int batch, int split) {
   const int forced = env_int("TIB_UPD_GROUP", 0);
-  if (forced > 0) return forced;
+  if (forced > 0) return std::min(forced, 16);  // two signals per term, <= 32 per task
   const bool chain_bound = split <= 0 && !batch_leaves(batch) && chain_work(F) <= env_int("TIB_SPLIT_WORK", 3000);
   return chain_bound ? 1 : 4;
 }
@@ -586,6 +586,10 @@ static void run_flow(DevPlan& P, const std::vector<BaseTable>& tables, cudaStrea
   a.agent = a.dedicate && a.static_chains && env_int("TIB_AGENT", 1) ? 1 : 0;
   a.poll_uploads = poll ? 1 : 0;
   a.c0_prefetch = P.c0_prefetch;
+  // early q1 tickets: launches of many matrices only (batch 236.1 -> 234.4 ms;
+  // large within noise, chain-bound medium 41.7 -> 43.4: a held ticket delays the
+  // critical item that lands in its slot)
+  a.early_ticket = env_int("TIB_EARLY_TICKET", batch_leaves(batch) ? 1 : 0);
   a.watchdog_ns = static_cast<unsigned long long>(env_int("TIB_WATCHDOG_S", 60)) * 1000000000ull;
   if (ta && batch == 1) {
     a.t_agents = ta->agents;

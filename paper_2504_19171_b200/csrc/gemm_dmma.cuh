@@ -166,7 +166,7 @@ static_assert(32 * kLdC0 <= 2 * kStageDoubles, "a ring stage holds half a C0 blo
 
 template <class Src>
 __device__ __forceinline__ int gemm_mainloop(const RTask& t, const Src& src, double* smem, double (&acc)[4][4][2],
-                                             bool prefetch_c0 = false) {
+                                             bool prefetch_c0 = false, int nchunks_hint = -1) {
   const int tid = wtid();
   const int lane = tid & 31, warp = tid >> 5;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
@@ -178,10 +178,14 @@ __device__ __forceinline__ int gemm_mainloop(const RTask& t, const Src& src, dou
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   // Flattened chunk sequence over segments, walked by a producer cursor.
-  int nchunks = 0;
-  for (int s = 0; s < src.count; ++s) {
-    const RSeg g = src.get(s);
-    nchunks += (g.k_hi - g.k_lo) / kBK;
+  // (plan tasks carry the count: no pass over the segments before the first load)
+  int nchunks = nchunks_hint;
+  if (nchunks < 0) {
+    nchunks = 0;
+    for (int s = 0; s < src.count; ++s) {
+      const RSeg g = src.get(s);
+      nchunks += (g.k_hi - g.k_lo) / kBK;
+    }
   }
   prefetch_c0 = prefetch_c0 && t.C0 != nullptr && nchunks >= 4;
   int ls = 0, lk = 0;

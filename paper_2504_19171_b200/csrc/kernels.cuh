@@ -40,6 +40,7 @@ struct FlowArgs {
   int agent;           // with dedicate + static_chains: the chain's sibling worker raises its signals
   int poll_uploads;    // streamed upload: tasks wait for their A-store column (DTask::poll)
   int c0_prefetch;     // plain tasks stage C0 in shared memory during their main loop
+  int early_ticket;    // bulk workers take their next q1 ticket once a task's waits are over (atomic latency hidden under the epilogue)
   // streamed two-chain upload (one matrix): worker 1 of the last t_agents CTAs
   // places the staged tiles of each column (upload order t_cols; entries
   // t_off[c] .. t_off[c+1]: Sigma-store slot t_src -> A-store slot t_dst,

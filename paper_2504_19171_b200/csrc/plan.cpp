@@ -161,6 +161,12 @@ struct Builder {
       }
     P.q0 = QueueDesc{0, n0, n0 > 0 ? crit_workers : 0, 0};
     P.q1 = QueueDesc{n0, static_cast<int>(P.tasks.size()) - n0, 0, 0};
+    for (DTask& t : P.tasks) {
+      t.chunks = 0;
+      if (t.kind == kGemmTask || t.kind == kSplitTask)
+        for (int k = t.seg_begin; k < t.seg_begin + t.seg_count; ++k)
+          t.chunks += (P.segs[static_cast<size_t>(k)].k_hi - P.segs[static_cast<size_t>(k)].k_lo) / kBK;
+    }
     finalize_waiters();
     return pos;
   }

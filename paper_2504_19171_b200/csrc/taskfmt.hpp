@@ -91,7 +91,8 @@ struct DTask {
   int seg_begin, seg_count;
   int dep_begin, sig_begin;
   int aux0, aux1;
-  int poll, pad2;  // streamed upload: counter (>= 1 once the A-store column the task touches is uploaded), or -1
+  int poll;    // streamed upload: counter (>= 1 once the A-store column the task touches is uploaded), or -1
+  int chunks;  // GEMM / split tasks: K chunks over all segments (set by the plan; the main loop needs no count pass)
   unsigned short dep_count, sig_count;
   unsigned char kind, mode, c_store, c0_store, cm_store, diag_store, dep2_count, sig2_count;
 };
