@@ -316,3 +316,22 @@ def test_watchdog_turns_a_stall_into_an_error(tib, monkeypatch):
     # the device stays usable
     res = tib.selected_inverse(tib.generate(700, 90, 12, 1.0, seed=5, tile_size=64), "pattern")
     assert np.all(res.diagonal() > 0)
+
+
+@pytest.mark.parametrize("group", ["1", "2", "16"])
+def test_grouped_updates_match_oracle(tib, orc, monkeypatch, group):
+    """Bulk update terms grouped 1 / 2 / 16 to a factor task (TIB_UPD_GROUP;
+    default 4) in the two-chain order and in a launch of 33 matrices (leaf
+    plans): Sigma, the marginal variances and the logdet match the oracle."""
+    monkeypatch.setenv("TIB_UPD_GROUP", group)
+    n, w, t, b = 6000, 700, 60, 128
+    ref = orc.selected_inverse_generated(n, w, t, 1.0, 7, b, "pattern")
+    m = tib.generate(n, w, t, 1.0, seed=7, tile_size=b)
+    assert tib.two_chain_order(m)[1] > 0
+    res = tib.selected_inverse(m, "pattern")
+    assert np.max(np.abs(res.diagonal() - ref["diag"]) / np.abs(ref["diag"])) <= 1e-10
+    assert abs(res.logdet() - ref["logdet"]) <= 1e-10 * abs(ref["logdet"])
+    ms = [m] + [tib.generate(n, w, t, 1.0, seed=100 + k, tile_size=b) for k in range(32)]
+    logdet, diag = tib.selected_inverse_batch(ms)
+    assert np.max(np.abs(diag[0] - ref["diag"]) / np.abs(ref["diag"])) <= 1e-10
+    assert abs(logdet[0] - ref["logdet"]) <= 1e-10 * abs(ref["logdet"])
