@@ -417,10 +417,10 @@ static int phase2_group(const Pattern& F, int batch, int split) {
 }
 
 // Reserved critical workers of a two-chain phase-2 plan: a throughput-bound
-// phase 2 (late terms grouped) needs few (large: 12 vs 24, 98.7 vs 99.8 ms), a
-// chain-bound one more (medium: 24 vs 12, 16.9 vs 17.7 ms).
+// phase 2 (late terms grouped) needs few (large: 8 vs 12, 97.9 vs 98.2 ms), a
+// chain-bound one more (medium: 32 vs 24, 16.4 vs 16.9 ms; profiles/r02_s4_ab_knobs.log).
 static int crit_split_p2(const Pattern& F, int split) {
-  return env_int("TIB_CRIT_SPLIT_P2", phase2_group(F, 1, split) > 1 ? 12 : 24);
+  return env_int("TIB_CRIT_SPLIT_P2", phase2_group(F, 1, split) > 1 ? 8 : 32);
 }
 
 static std::shared_ptr<Phase2Plan> phase2_plan_for(const Pattern& F, const Closure& sel, int device,

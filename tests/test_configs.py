@@ -115,8 +115,9 @@ def test_batch_config_vs_reference(tib, monkeypatch):
         check_against_golden(golden(name), 50000, 128, diag[k], logdet[k], None, None, None)
     # members are independent: one member alone (in the natural elimination
     # order, like the batch) gives the same bits
-    # (a batch runs plain leaf tasks and groups phase 2's late terms three to a
-    # part; a single call runs the chain task: the same values to rounding)
+    # (a batch runs plain leaf tasks, groups its bulk updates four to a task and
+    # phase 2's late terms eight to a part; a single call runs the chain task:
+    # the same values to rounding)
     monkeypatch.setenv("TIB_SPLIT", "0")
     single = tib.selected_inverse(ms[63], "pattern")
     assert abs(single.logdet() - logdet[63]) <= 1e-14 * abs(logdet[63])
